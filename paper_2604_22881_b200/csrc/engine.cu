@@ -1,0 +1,688 @@
+// GPU engine: executes the planner's BatchWork on the B200.
+//
+// Cross-stream hazards (everything else is ordered on `comp`):
+//   1. staging reuse   : H2D of batch i into staging[i%2] waits scatter(i-2)
+//   2. host chunk RAW  : H2D of a chunk waits the D2H event of the batch that wrote it
+//   3. offload slot    : gather into a reused offload slot waits the previous D2H
+// Pages themselves are only touched on `comp` (scatter, append, attention,
+// gather), so zero-copy eviction and page reuse need no synchronisation.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <random>
+
+namespace mtkv_b200 {
+
+#define CK(x)                                                   \
+  do {                                                          \
+    cudaError_t e_ = (x);                                       \
+    if (e_ != cudaSuccess) {                                    \
+      err = std::string(#x) + ": " + cudaGetErrorString(e_);    \
+      return MTKV_ERROR;                                        \
+    }                                                           \
+  } while (0)
+
+int DevBuf::ensure(size_t need) {
+  if (need <= bytes) return 0;
+  size_t nb = std::max(need, bytes * 2);
+  nb = (nb + 255) & ~size_t(255);
+  if (p) {
+    cudaDeviceSynchronize();
+    cudaFree(p);
+  }
+  p = nullptr;
+  bytes = 0;
+  if (cudaMalloc(&p, nb) != cudaSuccess) return -1;
+  bytes = nb;
+  return 0;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+__global__ void pick_scores_kernel(float* out, const float* logits, const uint32_t* creq,
+                                   const uint32_t* cid, uint32_t n, uint32_t vocab) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) out[j] = logits[(size_t)creq[j] * vocab + cid[j]];
+}
+
+Engine::Engine(const mtkv_kv_config& kv, const mtkv_cost_model& cost, const mtkv_engine_options& opt)
+    : planner(kv, cost, opt.mode, opt.backend == MTKV_BACKEND_VALUE), kv_(kv), opt_(opt) {
+  value_ = opt.backend == MTKV_BACKEND_VALUE;
+  recompute_ = opt.mode == MTKV_MODE_RECOMPUTE;
+  g_.L = kv.num_layers;
+  g_.H = kv.num_heads;
+  g_.D = kv.head_dim;
+  g_.d = kv.num_heads * kv.head_dim;
+  g_.S = kv.page_size;
+  g_.chunk = kv.chunk_size;
+  g_.num_pages = recompute_ ? 0 : kv.device_pages;
+  chunk_elems_ = size_t(g_.L) * 2 * g_.chunk * g_.d;
+  chunk_bytes_ = chunk_elems_ * sizeof(__nv_bfloat16);
+}
+
+Engine::~Engine() {
+  if (comp_) cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&pool_, &staging_[0], &staging_[1], &offload_, &meta_, &x_, &x2_, &u_, &q_,
+                    &mid_, &part_o_, &part_lse_, &logits_, &scores_};
+  for (DevBuf* b : bufs) b->release();
+  for (void* p : {(void*)w_embed_, (void*)w_in_, (void*)w1_, (void*)w2_, (void*)w_out_, (void*)w_ln_})
+    if (p) cudaFree(p);
+  for (char* s : slabs_) cudaFreeHost(s);
+  for (int k = 0; k < kRing; ++k) {
+    if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
+    if (scores_host_[k]) cudaFreeHost(scores_host_[k]);
+    if (logits_host_[k]) cudaFreeHost(logits_host_[k]);
+  }
+  if (comp_) {
+    for (int k = 0; k < kRing; ++k) {
+      cudaEventDestroy(ev_onload_[k]); cudaEventDestroy(ev_scatter_[k]);
+      cudaEventDestroy(ev_gathered_[k]); cudaEventDestroy(ev_d2h_[k]);
+      cudaEventDestroy(ev_done_[k]); cudaEventDestroy(ev_start_[k]);
+    }
+    for (auto e : ev_attn_) cudaEventDestroy(e);
+    cudaStreamDestroy(comp_); cudaStreamDestroy(h2d_); cudaStreamDestroy(d2h_);
+  }
+}
+
+// Reference weight init (model.cpp:34): mt19937_64(seed), N(0, 0.3/sqrt(d)) per
+// matrix in the order embed, per layer (w_in, ln_scale ~ N(0,1), w_mlp1, w_mlp2),
+// w_out; rounded to bf16 for the tensor cores (ln_scale kept fp32).
+void Engine::init_weights() {
+  const auto& mc = opt_.model;
+  const size_t d = g_.d, V = mc.vocab, L = g_.L;
+  std::mt19937_64 rng(mc.seed);
+  const double s = 0.3 / std::sqrt(double(d));
+  auto draw = [&](size_t n, double sd) {
+    std::normal_distribution<double> dist(0.0, sd);
+    std::vector<double> m(n);
+    for (auto& v : m) v = dist(rng);
+    return m;
+  };
+  auto to_bf16 = [](const std::vector<double>& m, std::vector<__nv_bfloat16>& out, size_t at) {
+    for (size_t i = 0; i < m.size(); ++i) out[at + i] = __float2bfloat16(float(m[i]));
+  };
+  std::vector<__nv_bfloat16> embed(V * d), w_in(L * d * 4 * d), w1(L * d * d), w2(L * d * d), w_out(d * V);
+  std::vector<float> ln(L * d);
+  to_bf16(draw(V * d, s), embed, 0);
+  for (size_t l = 0; l < L; ++l) {
+    to_bf16(draw(d * 4 * d, s), w_in, l * d * 4 * d);
+    auto lv = draw(d, 1.0);
+    for (size_t i = 0; i < d; ++i) ln[l * d + i] = float(lv[i]);
+    to_bf16(draw(d * d, s), w1, l * d * d);
+    to_bf16(draw(d * d, s), w2, l * d * d);
+  }
+  to_bf16(draw(d * V, s), w_out, 0);
+  auto up = [](auto& host, auto** dev) {
+    cudaMalloc((void**)dev, host.size() * sizeof(host[0]));
+    cudaMemcpy(*dev, host.data(), host.size() * sizeof(host[0]), cudaMemcpyHostToDevice);
+  };
+  up(embed, &w_embed_);
+  up(w_in, &w_in_);
+  up(w1, &w1_);
+  up(w2, &w2_);
+  up(w_out, &w_out_);
+  up(ln, &w_ln_);
+}
+
+int Engine::init(std::string& err) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    err = "no CUDA device available (the B200 engine has no CPU fallback)";
+    return MTKV_NO_DEVICE;
+  }
+  if (opt_.device < 0 || opt_.device >= ndev) {
+    err = "invalid CUDA device ordinal";
+    return MTKV_NO_DEVICE;
+  }
+  CK(cudaSetDevice(opt_.device));
+  if (g_.d % 2 != 0 || g_.d > 512) {
+    err = "engine: hidden width H*D must be even and <= 512";
+    return MTKV_ERROR;
+  }
+  if (g_.D > 128) {
+    err = "engine: head_dim must be <= 128";
+    return MTKV_ERROR;
+  }
+  if (kv_.bytes_per_element != 2) {
+    err = "engine: the device pool stores bf16 (bytes_per_element must be 2)";
+    return MTKV_ERROR;
+  }
+  CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  for (int k = 0; k < kRing; ++k) {
+    CK(cudaEventCreateWithFlags(&ev_onload_[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_scatter_[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_gathered_[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_d2h_[k], cudaEventDisableTiming));
+    CK(cudaEventCreate(&ev_done_[k]));
+    CK(cudaEventCreate(&ev_start_[k]));
+  }
+  if (!recompute_) {
+    if (pool_.ensure(size_t(g_.L) * g_.num_pages * 2 * g_.S * g_.d * sizeof(__nv_bfloat16))) {
+      err = "engine: cannot allocate the device page pool";
+      return MTKV_ERROR;
+    }
+    CK(cudaMemset(pool_.p, 0, pool_.bytes));
+  }
+  const uint64_t slots = std::max<uint64_t>(1, kv_.offload_quota / kv_.chunk_size);
+  if (!recompute_ && opt_.mode == MTKV_MODE_HIERARCHICAL) {
+    if (offload_.ensure(slots * chunk_bytes_)) {
+      err = "engine: cannot allocate the offload buffer";
+      return MTKV_ERROR;
+    }
+    off_free_.clear();
+    for (uint64_t s = slots; s-- > 0;) off_free_.push_back(uint32_t(s));
+    off_slot_batch_.assign(slots, -1);
+  }
+  slab_bytes_ = std::max<size_t>(size_t(256) << 20, chunk_bytes_ * 8);
+  slab_used_ = slab_bytes_;  // force a slab on first use
+  if (value_) init_weights();
+  CK(cudaGetLastError());
+  return MTKV_OK;
+}
+
+int Engine::host_chunk(uint64_t id, std::string& err) {
+  if (id < chunk_ptr_.size() && chunk_ptr_[id]) return MTKV_OK;
+  if (slab_used_ + chunk_bytes_ > slab_bytes_) {
+    char* s = nullptr;
+    CK(cudaHostAlloc((void**)&s, slab_bytes_, cudaHostAllocDefault));
+    slabs_.push_back(s);
+    slab_used_ = 0;
+  }
+  if (chunk_ptr_.size() <= id) {
+    chunk_ptr_.resize(id + 1, nullptr);
+    chunk_d2h_batch_.resize(id + 1, -1);
+    chunk_off_slot_.resize(id + 1, -1);
+  }
+  chunk_ptr_[id] = slabs_.back() + slab_used_;
+  slab_used_ += chunk_bytes_;
+  return MTKV_OK;
+}
+
+static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+template <class T>
+static T* carve(char* base, size_t& off, size_t count) {
+  T* p = reinterpret_cast<T*>(base + off);
+  off = align16(off + count * sizeof(T));
+  return p;
+}
+
+int Engine::process_batch(const mtkv_request* reqs, uint32_t n, std::string& err) {
+  CK(cudaSetDevice(opt_.device));
+  BatchWork w;
+  planner.plan_batch(reqs, n, w);
+  const int rc = enqueue(w, reqs, n, err);
+  if (w.rc) {
+    err = w.error;
+    planner.keep_last(w);
+    return w.rc;
+  }
+  planner.keep_last(w);
+  return rc;
+}
+
+int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, std::string& err) {
+  // completions that fired at batch start free their offload slots
+  for (uint64_t id : w.persisted) {
+    if (id < chunk_off_slot_.size() && chunk_off_slot_[id] >= 0) {
+      off_free_.push_back(uint32_t(chunk_off_slot_[id]));
+      chunk_off_slot_[id] = -1;
+    }
+  }
+  if (w.rc || n == 0) return MTKV_OK;
+  const int k = int(batch_no_ % kRing);
+  if (batch_no_ >= kRing) CK(cudaEventSynchronize(ev_done_[k]));  // ring slot free
+
+  const uint32_t S = g_.S, d = g_.d, H = g_.H, V = value_ ? opt_.model.vocab : 0;
+
+  // ---- recompute mode: transient pages for every fresh row ----
+  std::vector<uint32_t> tpages;
+  std::vector<uint32_t> t_off(n), t_np(n), t_soff(n), t_ns(n);
+  if (recompute_) {
+    uint32_t next = 0;
+    for (uint32_t r = 0; r < n; ++r) {
+      const auto& R = w.reqs[r];
+      t_off[r] = uint32_t(tpages.size());
+      t_np[r] = (R.n_hist + S - 1) / S;
+      for (uint32_t i = 0; i < t_np[r]; ++i) tpages.push_back(next++);
+      t_soff[r] = uint32_t(tpages.size());
+      t_ns[r] = (R.plan.num_candidates + S - 1) / S;
+      for (uint32_t i = 0; i < t_ns[r]; ++i) tpages.push_back(next++);
+    }
+    if (next > g_.num_pages) {
+      g_.num_pages = std::max<uint32_t>(next, g_.num_pages * 2);
+      if (pool_.ensure(size_t(g_.L) * g_.num_pages * 2 * S * d * sizeof(__nv_bfloat16))) {
+        err = "engine: cannot grow the transient page pool";
+        return MTKV_ERROR;
+      }
+    }
+  }
+  const std::vector<uint32_t>& pages = recompute_ ? tpages : w.pages;
+
+  // ---- rows, attention work, metadata sizes ----
+  std::vector<ReqDev> rd(n);
+  uint32_t rows = 0, part_rows = 0, max_hist = 0, n_items = 0, ncand_total = 0;
+  constexpr uint32_t kSplitKeys = 512;
+  for (uint32_t r = 0; r < n; ++r) {
+    const ReqWork& R = w.reqs[r];
+    ReqDev& x = rd[r];
+    x.q_row0 = rows;
+    x.n_hist = R.n_hist;
+    x.n_cand = R.plan.num_candidates;
+    x.n_q = x.n_hist + x.n_cand;
+    x.start = R.start;
+    x.pages_off = recompute_ ? t_off[r] : R.pages_off;
+    x.n_pages = recompute_ ? t_np[r] : R.n_pages;
+    x.scratch_off = recompute_ ? t_soff[r] : R.scratch_off;
+    x.n_scratch = recompute_ ? t_ns[r] : R.n_scratch;
+    x.user = R.plan.user;
+    const uint64_t T = x.start + x.n_q;
+    x.split_keys = x.n_q <= 128 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 64, 0xFFFFFFFFull));
+    x.n_splits = uint32_t((T + x.split_keys - 1) / x.split_keys);
+    x.part_base = part_rows;
+    part_rows += x.n_splits * x.n_q;
+    const uint32_t bq = 64;
+    n_items += H * ((x.n_q + bq - 1) / bq) * x.n_splits;
+    rows += x.n_q;
+    ncand_total += x.n_cand;
+    max_hist = std::max(max_hist, x.n_hist);
+  }
+  const uint32_t n_on = uint32_t(w.onloads.size()), n_off = uint32_t(w.offloads.size());
+
+  size_t need = 0;
+  need = align16(need + n * sizeof(ReqDev));
+  need = align16(need + pages.size() * sizeof(uint32_t));
+  need = align16(need + rows * sizeof(uint32_t));      // tok
+  need = align16(need + rows * sizeof(uint64_t));      // kv_off
+  need = align16(need + rows * sizeof(uint32_t));      // row_req
+  need = align16(need + n * sizeof(uint32_t));         // last_row
+  need = align16(need + n_items * sizeof(AttnItem));
+  need = align16(need + (n_on + n_off) * sizeof(ChunkWork));
+  need = align16(need + 2 * ncand_total * sizeof(uint32_t));
+  if (meta_host_bytes_[k] < need) {
+    if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
+    meta_host_bytes_[k] = std::max(need, meta_host_bytes_[k] * 2);
+    CK(cudaHostAlloc((void**)&meta_host_[k], meta_host_bytes_[k], cudaHostAllocDefault));
+  }
+  if (meta_.ensure(need * kRing)) { err = "engine: metadata alloc"; return MTKV_ERROR; }
+  char* hb = meta_host_[k];
+  char* db = static_cast<char*>(meta_.p) + size_t(k) * (meta_.bytes / kRing);
+  if (need > meta_.bytes / kRing) { err = "engine: metadata ring overflow"; return MTKV_ERROR; }
+  size_t off = 0;
+  ReqDev* h_req = carve<ReqDev>(hb, off, n);
+  const size_t o_pages = off;
+  uint32_t* h_pages = carve<uint32_t>(hb, off, pages.size());
+  const size_t o_tok = off;
+  uint32_t* h_tok = carve<uint32_t>(hb, off, rows);
+  const size_t o_kv = off;
+  uint64_t* h_kv = carve<uint64_t>(hb, off, rows);
+  const size_t o_rr = off;
+  uint32_t* h_rr = carve<uint32_t>(hb, off, rows);
+  const size_t o_last = off;
+  uint32_t* h_last = carve<uint32_t>(hb, off, n);
+  const size_t o_items = off;
+  AttnItem* h_items = carve<AttnItem>(hb, off, n_items);
+  const size_t o_chunks = off;
+  ChunkWork* h_chunks = carve<ChunkWork>(hb, off, n_on + n_off);
+  const size_t o_cand = off;
+  uint32_t* h_creq = carve<uint32_t>(hb, off, ncand_total);
+  uint32_t* h_cid = h_creq + ncand_total;
+  off = align16(o_cand + 2 * ncand_total * sizeof(uint32_t));
+
+  std::memcpy(h_req, rd.data(), n * sizeof(ReqDev));
+  if (!pages.empty()) std::memcpy(h_pages, pages.data(), pages.size() * sizeof(uint32_t));
+  last_cands_.clear();
+  last_nc_.assign(n, 0);
+  uint32_t it = 0, cj = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    const ReqDev& x = rd[r];
+    const ReqWork& R = w.reqs[r];
+    for (uint32_t i = 0; i < x.n_q; ++i) {
+      const uint32_t row = x.q_row0 + i;
+      h_rr[row] = r;
+      h_tok[row] = value_ ? w.tokens[R.tok_off + i] : 0;
+      uint32_t page, slot;
+      if (i < x.n_hist) {
+        const uint64_t pos = x.start + i;
+        page = pages[x.pages_off + uint32_t(pos / S)];
+        slot = uint32_t(pos % S);
+      } else {
+        const uint32_t c = i - x.n_hist;
+        page = pages[x.scratch_off + c / S];
+        slot = c % S;
+      }
+      h_kv[row] = (uint64_t(page) * 2 * S + slot) * d;
+    }
+    h_last[r] = x.q_row0 + x.n_q - 1;
+    for (uint32_t h = 0; h < H; ++h)
+      for (uint32_t qt = 0; qt < (x.n_q + 63) / 64; ++qt)
+        for (uint32_t s = 0; s < x.n_splits; ++s) h_items[it++] = AttnItem{r, h, qt, s};
+    last_nc_[r] = x.n_cand;
+    for (uint32_t c = 0; c < x.n_cand; ++c) {
+      const uint32_t id = value_ ? w.tokens[R.tok_off + x.n_hist + c] : 0;
+      h_creq[cj] = r;
+      h_cid[cj] = id;
+      last_cands_.push_back(id);
+      ++cj;
+    }
+  }
+  for (uint32_t j = 0; j < n_on; ++j) h_chunks[j] = ChunkWork{j, w.onloads[j].pages_off};
+  std::vector<uint32_t> off_slots(n_off);
+  for (uint32_t j = 0; j < n_off; ++j) {
+    if (off_free_.empty()) { err = "engine: offload slots exhausted (quota accounting broken)"; return MTKV_ERROR; }
+    off_slots[j] = off_free_.back();
+    off_free_.pop_back();
+    h_chunks[n_on + j] = ChunkWork{off_slots[j], w.offloads[j].pages_off};
+  }
+
+  // ---- onload: copy-engine H2D into staging[batch % 2] ----
+  const int sb = int(batch_no_ % 2);
+  if (n_on) {
+    if (staging_slots_ < n_on || !staging_[sb].p || staging_[sb].bytes < size_t(n_on) * chunk_bytes_) {
+      if (staging_[sb].ensure(size_t(n_on) * chunk_bytes_)) { err = "engine: staging alloc"; return MTKV_ERROR; }
+    }
+    if (batch_no_ >= 2) CK(cudaStreamWaitEvent(h2d_, ev_scatter_[(batch_no_ - 2) % kRing], 0));
+    int64_t waited = -1;
+    for (uint32_t j = 0; j < n_on; ++j) {
+      const ChunkMove& m = w.onloads[j];
+      if (m.chunk_id >= chunk_ptr_.size() || !chunk_ptr_[m.chunk_id]) {
+        err = "engine: onload of a chunk with no host copy";
+        return MTKV_ERROR;
+      }
+      const int64_t b = chunk_d2h_batch_[m.chunk_id];
+      if (b >= 0 && b > waited) {
+        CK(cudaStreamWaitEvent(h2d_, ev_d2h_[b % kRing], 0));
+        waited = b;
+      }
+      CK(cudaMemcpyAsync(static_cast<char*>(staging_[sb].p) + size_t(j) * chunk_bytes_, chunk_ptr_[m.chunk_id],
+                         chunk_bytes_, cudaMemcpyHostToDevice, h2d_));
+    }
+    CK(cudaEventRecord(ev_onload_[k], h2d_));
+    h2d_bytes_ += uint64_t(n_on) * chunk_bytes_;
+    onload_chunks_ += n_on;
+  }
+
+  // ---- compute stream ----
+  CK(cudaEventRecord(ev_start_[k], comp_));
+  CK(cudaMemcpyAsync(db, hb, off, cudaMemcpyHostToDevice, comp_));
+  h2d_bytes_ += off;
+  const ReqDev* d_req = reinterpret_cast<const ReqDev*>(db);
+  const uint32_t* d_pages = reinterpret_cast<const uint32_t*>(db + o_pages);
+  const uint32_t* d_tok = reinterpret_cast<const uint32_t*>(db + o_tok);
+  const uint64_t* d_kv = reinterpret_cast<const uint64_t*>(db + o_kv);
+  const uint32_t* d_rr = reinterpret_cast<const uint32_t*>(db + o_rr);
+  const uint32_t* d_last = reinterpret_cast<const uint32_t*>(db + o_last);
+  const AttnItem* d_items = reinterpret_cast<const AttnItem*>(db + o_items);
+  const ChunkWork* d_chunks = reinterpret_cast<const ChunkWork*>(db + o_chunks);
+  const uint32_t* d_creq = reinterpret_cast<const uint32_t*>(db + o_cand);
+  const uint32_t* d_cid = d_creq + ncand_total;
+  __nv_bfloat16* pool = static_cast<__nv_bfloat16*>(pool_.p);
+
+  if (n_on) {
+    CK(cudaStreamWaitEvent(comp_, ev_onload_[k], 0));
+    launch_scatter_chunks(pool, static_cast<const __nv_bfloat16*>(staging_[sb].p), d_chunks, d_pages, n_on, g_, comp_);
+    ++launches;
+  }
+  CK(cudaEventRecord(ev_scatter_[k], comp_));
+
+  attn_launches_last_ = 0;
+  if (value_) {
+    const size_t rb = size_t(rows) * d * sizeof(__nv_bfloat16);
+    if (x_.ensure(rb) || x2_.ensure(rb) || u_.ensure(rb) || q_.ensure(rb) || mid_.ensure(rb) ||
+        part_o_.ensure(size_t(part_rows) * d * sizeof(float)) ||
+        part_lse_.ensure(size_t(part_rows) * H * sizeof(float)) ||
+        logits_.ensure(size_t(n) * V * sizeof(float)) || scores_.ensure(size_t(ncand_total) * sizeof(float))) {
+      err = "engine: workspace alloc";
+      return MTKV_ERROR;
+    }
+    auto* X = static_cast<__nv_bfloat16*>(x_.p);
+    auto* X2 = static_cast<__nv_bfloat16*>(x2_.p);
+    auto* U = static_cast<__nv_bfloat16*>(u_.p);
+    auto* Q = static_cast<__nv_bfloat16*>(q_.p);
+    auto* MID = static_cast<__nv_bfloat16*>(mid_.p);
+    launch_embed(X, w_embed_, d_tok, rows, d, comp_);
+    ++launches;
+    const bool prof = opt_.profile != 0;
+    if (prof && ev_attn_.size() < 2 * g_.L) {
+      while (ev_attn_.size() < 2 * g_.L) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ev_attn_.push_back(e);
+      }
+    }
+    for (uint32_t l = 0; l < g_.L; ++l) {
+      GemmArgs ga{};
+      ga.A = X; ga.B = w_in_ + size_t(l) * d * 4 * d; ga.M = rows; ga.N = 4 * d; ga.K = d;
+      ga.epi = Epi::Proj; ga.out_u = U; ga.out_q = Q; ga.pool = pool; ga.kv_off = d_kv;
+      ga.layer_base = size_t(l) * g_.num_pages * 2 * S * d; ga.d = d; ga.kv_stride = S * d;
+      launch_gemm(ga, comp_);
+      AttnArgs aa{};
+      aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.items = d_items; aa.n_items = n_items;
+      aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
+      aa.g = g_; aa.layer = l; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
+      if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
+      launch_attention(aa, comp_);
+      if (prof) CK(cudaEventRecord(ev_attn_[2 * l + 1], comp_));
+      ++attn_launches_last_;
+      GateArgs gn{};
+      gn.part_o = aa.part_o; gn.part_lse = aa.part_lse; gn.u = U; gn.ln_scale = w_ln_ + size_t(l) * d;
+      gn.row_req = d_rr; gn.reqs = d_req; gn.out = X2; gn.rows = rows; gn.H = H; gn.D = g_.D;
+      launch_gate_norm(gn, comp_);
+      GemmArgs m1{};
+      m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = rows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID;
+      launch_gemm(m1, comp_);
+      GemmArgs m2{};
+      m2.A = MID; m2.B = w2_ + size_t(l) * d * d; m2.M = rows; m2.N = d; m2.K = d; m2.epi = Epi::Bf16; m2.out = X;
+      launch_gemm(m2, comp_);
+      launches += 5;
+    }
+    GemmArgs hd{};
+    hd.A = X; hd.row_idx = d_last; hd.B = w_out_; hd.M = n; hd.N = V; hd.K = d; hd.epi = Epi::F32; hd.out = logits_.p;
+    launch_gemm(hd, comp_);
+    ++launches;
+    if (ncand_total) {
+      pick_scores_kernel<<<(ncand_total + 127) / 128, 128, 0, comp_>>>(
+          static_cast<float*>(scores_.p), static_cast<const float*>(logits_.p), d_creq, d_cid, ncand_total, V);
+      ++launches;
+      if (scores_host_bytes_[k] < ncand_total * sizeof(float)) {
+        if (scores_host_[k]) cudaFreeHost(scores_host_[k]);
+        scores_host_bytes_[k] = std::max<size_t>(ncand_total * sizeof(float), 4096);
+        CK(cudaHostAlloc((void**)&scores_host_[k], scores_host_bytes_[k], cudaHostAllocDefault));
+      }
+      CK(cudaMemcpyAsync(scores_host_[k], scores_.p, ncand_total * sizeof(float), cudaMemcpyDeviceToHost, comp_));
+      d2h_bytes_ += ncand_total * sizeof(float);
+    }
+    if (opt_.keep_logits) {
+      const size_t lb = size_t(n) * V * sizeof(float);
+      if (logits_host_bytes_[k] < lb) {
+        if (logits_host_[k]) cudaFreeHost(logits_host_[k]);
+        logits_host_bytes_[k] = lb;
+        CK(cudaHostAlloc((void**)&logits_host_[k], lb, cudaHostAllocDefault));
+      }
+      CK(cudaMemcpyAsync(logits_host_[k], logits_.p, lb, cudaMemcpyDeviceToHost, comp_));
+      d2h_bytes_ += lb;
+    }
+  } else {
+    launch_tag_append(pool, d_req, d_pages, n, max_hist, g_, comp_);
+    ++launches;
+  }
+
+  // ---- offload: gather on comp (pages only ever touched here), D2H on d2h ----
+  if (n_off) {
+    int64_t waited = -1;
+    for (uint32_t j = 0; j < n_off; ++j) {
+      const int64_t b = off_slot_batch_[off_slots[j]];
+      if (b >= 0 && b > waited) {
+        CK(cudaStreamWaitEvent(comp_, ev_d2h_[b % kRing], 0));
+        waited = b;
+      }
+    }
+    launch_gather_chunks(static_cast<__nv_bfloat16*>(offload_.p), pool, d_chunks + n_on, d_pages, n_off, g_, comp_);
+    ++launches;
+    CK(cudaEventRecord(ev_gathered_[k], comp_));
+    CK(cudaStreamWaitEvent(d2h_, ev_gathered_[k], 0));
+    for (uint32_t j = 0; j < n_off; ++j) {
+      const ChunkMove& m = w.offloads[j];
+      if (host_chunk(m.chunk_id, err)) return MTKV_ERROR;
+      CK(cudaMemcpyAsync(chunk_ptr_[m.chunk_id], static_cast<char*>(offload_.p) + size_t(off_slots[j]) * chunk_bytes_,
+                         chunk_bytes_, cudaMemcpyDeviceToHost, d2h_));
+      chunk_d2h_batch_[m.chunk_id] = int64_t(batch_no_);
+      chunk_off_slot_[m.chunk_id] = off_slots[j];
+      off_slot_batch_[off_slots[j]] = int64_t(batch_no_);
+    }
+    CK(cudaEventRecord(ev_d2h_[k], d2h_));
+    d2h_bytes_ += uint64_t(n_off) * chunk_bytes_;
+    offload_chunks_ += n_off;
+  }
+  CK(cudaEventRecord(ev_done_[k], comp_));
+  CK(cudaGetLastError());
+  last_slot_ = k;
+  last_n_ = n;
+  ++batch_no_;
+  return MTKV_OK;
+}
+
+int Engine::drain(std::string& err) {
+  std::vector<uint64_t> persisted;
+  planner.drain(&persisted);
+  for (uint64_t id : persisted)
+    if (id < chunk_off_slot_.size() && chunk_off_slot_[id] >= 0) {
+      off_free_.push_back(uint32_t(chunk_off_slot_[id]));
+      chunk_off_slot_[id] = -1;
+    }
+  (void)err;
+  return MTKV_OK;
+}
+
+int Engine::synchronize(std::string& err) {
+  CK(cudaSetDevice(opt_.device));
+  CK(cudaStreamSynchronize(comp_));
+  CK(cudaStreamSynchronize(h2d_));
+  CK(cudaStreamSynchronize(d2h_));
+  return MTKV_OK;
+}
+
+int Engine::last_logits(float* out, uint32_t cap_rows, std::string& err) {
+  if (!value_) { err = "logits: tag backend has no model"; return MTKV_ERROR; }
+  if (!opt_.keep_logits) { err = "logits: engine created without keep_logits"; return MTKV_ERROR; }
+  if (last_slot_ < 0) return 0;
+  CK(cudaEventSynchronize(ev_done_[last_slot_]));
+  const uint32_t rows = std::min(cap_rows, last_n_);
+  std::memcpy(out, logits_host_[last_slot_], size_t(rows) * opt_.model.vocab * sizeof(float));
+  return int(last_n_);
+}
+
+int Engine::last_rankings(uint32_t* out, uint64_t cap, std::string& err) {
+  if (!value_) { err = "rankings: tag backend has no model"; return MTKV_ERROR; }
+  if (last_slot_ < 0) return 0;
+  CK(cudaEventSynchronize(ev_done_[last_slot_]));
+  const float* sc = scores_host_[last_slot_];
+  uint64_t o = 0;
+  size_t base = 0;
+  for (uint32_t r = 0; r < last_n_; ++r) {
+    std::vector<uint32_t> idx(last_nc_[r]);
+    for (uint32_t i = 0; i < last_nc_[r]; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return sc[base + a] > sc[base + b]; });
+    for (uint32_t i : idx)
+      if (o < cap) out[o++] = last_cands_[base + i];
+    base += last_nc_[r];
+  }
+  return int(o);
+}
+
+int64_t Engine::read_user_kv(uint32_t user, uint32_t layer, uint16_t* kout, uint16_t* vout, uint64_t cap,
+                             std::string& err) {
+  if (synchronize(err)) return -1;
+  const UserRec* u = planner.find(user);
+  if (!u || !u->known) { err = "read_user_kv: unknown user"; return -1; }
+  if (layer >= g_.L) { err = "read_user_kv: bad layer"; return -1; }
+  const uint64_t n = std::min<uint64_t>(u->device_len, cap);
+  const size_t seg = size_t(g_.S) * g_.d;
+  std::vector<uint16_t> buf(2 * seg);
+  for (uint64_t pos = 0; pos < n; pos += g_.S) {
+    const uint32_t page = u->pages[pos / g_.S];
+    const size_t o = g_.off(layer, page, 0, 0);
+    if (cudaMemcpy(buf.data(), static_cast<__nv_bfloat16*>(pool_.p) + o, 2 * seg * 2, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      err = "read_user_kv: copy failed";
+      return -1;
+    }
+    const uint64_t take = std::min<uint64_t>(g_.S, n - pos);
+    std::memcpy(kout + pos * g_.d, buf.data(), take * g_.d * 2);
+    std::memcpy(vout + pos * g_.d, buf.data() + seg, take * g_.d * 2);
+  }
+  return int64_t(n);
+}
+
+int Engine::check_conservation(std::string& err) {
+  if (value_) { err = "conservation check uses the tag backend"; return MTKV_ERROR; }
+  if (synchronize(err)) return MTKV_ERROR;
+  const uint32_t L = g_.L, d = g_.d, C = g_.chunk;
+  for (uint32_t uid : planner.known_users()) {
+    const UserRec* u = planner.find(uid);
+    if (u->persisted_len % C) { err = "conservation: persisted length not chunk-aligned"; return MTKV_ERROR; }
+    if (u->pages.size() * uint64_t(g_.S) < u->device_len) { err = "conservation: device length exceeds page table"; return MTKV_ERROR; }
+    std::vector<uint16_t> kb(u->device_len * d + 1), vb(u->device_len * d + 1);
+    for (uint32_t l = 0; l < L; ++l) {
+      if (read_user_kv(uid, l, kb.data(), vb.data(), u->device_len, err) < 0) return MTKV_ERROR;
+      for (uint64_t pos = 0; pos < u->device_len; ++pos)
+        for (uint32_t j = 0; j < d; ++j)
+          if (kb[pos * d + j] != tag_word(uid, pos, l, 0, j) || vb[pos * d + j] != tag_word(uid, pos, l, 1, j)) {
+            err = "conservation: wrong identity on device (user " + std::to_string(uid) + ", pos " +
+                  std::to_string(pos) + ", layer " + std::to_string(l) + ")";
+            return MTKV_ERROR;
+          }
+    }
+    if (u->host_chunks.size() != u->persisted_len / C) { err = "conservation: host chunk count disagrees"; return MTKV_ERROR; }
+    for (size_t c = 0; c < u->host_chunks.size(); ++c) {
+      const uint16_t* hc = reinterpret_cast<const uint16_t*>(chunk_ptr_[u->host_chunks[c]]);
+      for (uint32_t l = 0; l < L; ++l)
+        for (uint32_t kv = 0; kv < 2; ++kv)
+          for (uint32_t t = 0; t < C; ++t)
+            for (uint32_t j = 0; j < d; ++j)
+              if (hc[((size_t(l) * 2 + kv) * C + t) * d + j] != tag_word(uid, c * C + t, l, kv, j)) {
+                err = "conservation: wrong identity on host (user " + std::to_string(uid) + ")";
+                return MTKV_ERROR;
+              }
+    }
+  }
+  return MTKV_OK;
+}
+
+double Engine::last_batch_ms() {
+  if (last_slot_ < 0) return 0;
+  cudaEventSynchronize(ev_done_[last_slot_]);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev_start_[last_slot_], ev_done_[last_slot_]);
+  return ms;
+}
+
+double Engine::last_attention_ms(uint32_t* n) {
+  if (n) *n = attn_launches_last_;
+  if (last_slot_ < 0 || !opt_.profile || ev_attn_.empty()) return 0;
+  cudaEventSynchronize(ev_done_[last_slot_]);
+  double tot = 0;
+  for (uint32_t l = 0; l < attn_launches_last_ && 2 * l + 1 < ev_attn_.size(); ++l) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_attn_[2 * l], ev_attn_[2 * l + 1]);
+    tot += ms;
+  }
+  return tot;
+}
+
+void Engine::report(mtkv_run_report& r) const {
+  planner.report(r);
+  r.h2d_bytes = h2d_bytes_;
+  r.d2h_bytes = d2h_bytes_;
+  r.onload_chunks = onload_chunks_;
+  r.offload_chunks = offload_chunks_;
+}
+
+}  // namespace mtkv_b200

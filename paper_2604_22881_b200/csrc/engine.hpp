@@ -1,0 +1,103 @@
+// GPU engine = Planner (host control plane) + executor (B200 data plane).
+//
+// Streams (paper §4.4 four lanes, mapped onto B200 engines):
+//   comp : scatter, per-layer GEMM/append/attention/norm, logits, offload gathers
+//   h2d  : copy-engine onload of host chunks into a staging slot ring
+//   d2h  : copy-engine offload of gathered chunks into the pinned host store
+// The planner never waits for the device, so the onload copies of batch i+1
+// are enqueued while batch i still computes (cross-batch overlap); the only
+// cross-stream edges are the three hazards documented in engine.cu.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "planner.hpp"
+
+namespace mtkv_b200 {
+
+constexpr int kRing = 4;  // batches in flight on the device
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need);  // grows (device-synchronising) when needed
+  void release();
+};
+
+class Engine {
+ public:
+  Engine(const mtkv_kv_config& kv, const mtkv_cost_model& cost, const mtkv_engine_options& opt);
+  ~Engine();
+  int init(std::string& err);
+
+  int process_batch(const mtkv_request* reqs, uint32_t n, std::string& err);
+  int drain(std::string& err);
+  int synchronize(std::string& err);
+  int last_logits(float* out, uint32_t cap_rows, std::string& err);
+  int last_rankings(uint32_t* out, uint64_t cap, std::string& err);
+  int check_conservation(std::string& err);
+  int64_t read_user_kv(uint32_t user, uint32_t layer, uint16_t* k, uint16_t* v, uint64_t cap,
+                       std::string& err);
+  double last_batch_ms();
+  double last_attention_ms(uint32_t* launches);
+  void report(mtkv_run_report& r) const;
+  uint32_t batch_size() const { return opt_.batch_size ? opt_.batch_size : 1; }
+
+  Planner planner;
+  uint64_t launches = 0;
+
+ private:
+  int enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, std::string& err);
+  int host_chunk(uint64_t id, std::string& err);  // ensure pinned storage for chunk id
+  void init_weights();
+
+  mtkv_kv_config kv_;
+  mtkv_engine_options opt_;
+  PoolGeom g_{};
+  size_t chunk_elems_ = 0, chunk_bytes_ = 0;
+  bool value_ = false, recompute_ = false;
+
+  cudaStream_t comp_ = nullptr, h2d_ = nullptr, d2h_ = nullptr;
+  cudaEvent_t ev_onload_[kRing], ev_scatter_[kRing], ev_gathered_[kRing], ev_d2h_[kRing],
+      ev_done_[kRing], ev_start_[kRing];
+  std::vector<cudaEvent_t> ev_attn_;  // profiling pairs of the last batch
+  uint32_t attn_launches_last_ = 0;
+  uint64_t batch_no_ = 0;
+  int64_t last_slot_ = -1;
+  bool have_scatter_[kRing] = {false, false, false, false};
+  bool have_d2h_[kRing] = {false, false, false, false};
+  int64_t scatter_batch_[kRing] = {-1, -1, -1, -1};
+
+  // device memory
+  DevBuf pool_, staging_[2], offload_, meta_, x_, x2_, u_, q_, mid_, part_o_, part_lse_, logits_, scores_;
+  __nv_bfloat16 *w_embed_ = nullptr, *w_in_ = nullptr, *w1_ = nullptr, *w2_ = nullptr, *w_out_ = nullptr;
+  float* w_ln_ = nullptr;
+  uint32_t staging_slots_ = 0;
+
+  // pinned host memory
+  std::vector<char*> slabs_;
+  size_t slab_bytes_ = 0, slab_used_ = 0;
+  std::vector<char*> chunk_ptr_;          // chunk id -> pinned [L][2][chunk][d]
+  std::vector<int64_t> chunk_d2h_batch_;  // batch whose d2h ring event covers the chunk
+  std::vector<uint32_t> off_free_;        // free offload slots
+  std::vector<int64_t> off_slot_batch_;   // last batch that used each offload slot
+  std::vector<int64_t> chunk_off_slot_;   // chunk id -> offload slot while in flight
+  char* meta_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
+  size_t meta_host_bytes_[kRing] = {0, 0, 0, 0};
+  float* scores_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
+  size_t scores_host_bytes_[kRing] = {0, 0, 0, 0};
+  float* logits_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
+  size_t logits_host_bytes_[kRing] = {0, 0, 0, 0};
+
+  // last batch bookkeeping for logits / rankings
+  uint32_t last_n_ = 0;
+  std::vector<uint32_t> last_cands_, last_nc_;
+  uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0, onload_chunks_ = 0, offload_chunks_ = 0;
+};
+
+}  // namespace mtkv_b200

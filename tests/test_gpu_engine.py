@@ -1,0 +1,216 @@
+"""GPU parity tests (B200): the engine's data plane through the C-ABI against
+the reference fixtures and the C oracle.
+
+Bars (stated here, as DESIGN.md §(c)):
+  * control plane: bit-exact (state digest after every batch);
+  * data movement (tag backend): bit-exact — every byte of every resident
+    token on device and of every persisted host chunk is checked;
+  * numerics (value backend, bf16 storage / fp32 accumulate vs fp64 reference):
+    per request max|dlogit| <= LOGIT_TOL * max(1, max|logit|); K/V max abs
+    error <= KV_TOL * max|kv|; attention op vs torch fp32 <= ATTN_TOL abs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_22881_b200 as mtkv
+from oracle.oracle import ModelParams
+from tests.util import REPORT_KEYS, batches, golden_cases, state_digest
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 0.05
+KV_TOL = 0.03
+ATTN_TOL = 2e-2
+
+
+def _kv(d):
+    return mtkv.KVConfig(**{**mtkv.KVConfig().__dict__, **d})
+
+
+def _bf16_bits_to_f32(a: np.ndarray) -> np.ndarray:
+    return (a.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("case", golden_cases("tag"), ids=lambda c: c["name"])
+def test_tag_engine_bit_exact(case):
+    for run in case["runs"]:
+        eng = mtkv.Engine(_kv(case["kv"]), mode=run["mode"], backend="tag", batch_size=run["batch_size"])
+        for i, b in enumerate(batches(case["trace"], run["batch_size"])):
+            rej = False
+            try:
+                eng.process_batch(b)
+            except mtkv.BatchRejected:
+                rej = True
+            assert rej == run["rejected"][i]
+            assert state_digest(eng.state()) == run["digests"][i]
+            if run["mode"] != "recompute":
+                eng.check_conservation()  # reads back pool + host store, every byte
+        eng.drain()
+        assert eng.state() == run["final_state"]
+        if run["mode"] != "recompute":
+            eng.check_conservation()
+        rep = eng.report()
+        for k in REPORT_KEYS:
+            assert rep[k] == run["report"][k], k
+        assert eng.kernel_launches() > 0
+
+
+def _rel_logit_err(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+@pytest.mark.parametrize("case", golden_cases("value"), ids=lambda c: c["name"])
+def test_value_engine_logits_match_reference(case):
+    m = mtkv.ModelConfig(**case["model"])
+    for run in case["runs"]:
+        eng = mtkv.Engine(_kv(case["kv"]), mode=run["mode"], backend="value", batch_size=run["batch_size"],
+                          model=m, keep_logits=True)
+        got = []
+        for i, b in enumerate(batches(case["trace"], run["batch_size"])):
+            eng.process_batch(b)
+            assert state_digest(eng.state()) == run["digests"][i]
+            got.extend(eng.last_logits().tolist())
+        ref = np.array(run["logits"])
+        got = np.array(got)
+        assert got.shape == ref.shape
+        worst = max(_rel_logit_err(g, r) for g, r in zip(got, ref))
+        print(f"{case['name']} {run['mode']} bs{run['batch_size']}: worst rel logit err {worst:.3e}")
+        assert worst <= LOGIT_TOL
+
+
+def test_value_engine_kv_matches_oracle():
+    """K/V appended into the paged pool (and onloaded back) vs the fp64 oracle."""
+    case = [c for c in golden_cases("value") if c["name"] == "value_d64"][0]
+    m = mtkv.ModelConfig(**case["model"])
+    eng = mtkv.Engine(_kv(case["kv"]), mode="hierarchical", backend="value", batch_size=2, model=m)
+    hist = {}
+    for b in batches(case["trace"], 2):
+        eng.process_batch(b)
+        for r in b:
+            hist.setdefault(r["user"], []).extend(r["tokens"])
+    eng.synchronize()
+    p = ModelParams(**case["model"])
+    checked = 0
+    for u in eng.known_users():
+        n = eng.user_state(u)["device_len"]
+        if n == 0:
+            continue
+        _, nk, nv = p.forward(hist[u][:n], [0])
+        for layer in range(case["kv"]["num_layers"]):
+            k, v = eng.read_user_kv(u, layer)
+            kf, vf = _bf16_bits_to_f32(k), _bf16_bits_to_f32(v)
+            rk, rv = nk[layer, :n], nv[layer, :n]
+            assert np.abs(kf - rk).max() <= KV_TOL * max(1e-3, np.abs(rk).max())
+            assert np.abs(vf - rv).max() <= KV_TOL * max(1e-3, np.abs(rv).max())
+        checked += 1
+    assert checked > 0
+
+
+def test_value_engine_rankings():
+    """rank_candidates (model.cpp:199) on top of the GPU scores."""
+    case = [c for c in golden_cases("value") if c["name"] == "value10"][0]
+    m = mtkv.ModelConfig(**case["model"])
+    run = case["runs"][0]
+    eng = mtkv.Engine(_kv(case["kv"]), mode=run["mode"], backend="value", batch_size=1, model=m,
+                      keep_logits=True)
+    agree = total = 0
+    for i, b in enumerate(batches(case["trace"], 1)):
+        eng.process_batch(b)
+        ranked = eng.last_rankings()[0]
+        ref_logits = run["logits"][i]
+        want = mtkv.rank_candidates(ref_logits, b[0]["cands"])
+        margin = min((abs(ref_logits[x] - ref_logits[y]) for x in b[0]["cands"] for y in b[0]["cands"]
+                      if x != y and ref_logits[x] != ref_logits[y]), default=1.0)
+        if margin > 0.05:  # orderings decided by more than the bf16 error bar must agree exactly
+            total += 1
+            agree += ranked == want
+    assert total > 0 and agree == total
+
+
+def test_model_dims_of_bench_config():
+    """d = 256 (H=2, D=128): vector/tensor-core paths at the bench width vs the oracle."""
+    kv = dict(num_layers=2, num_heads=2, head_dim=128, page_size=32, chunk_size=64, device_pages=64,
+              offload_quota=256)
+    mc = dict(num_layers=2, num_heads=2, head_dim=128, vocab=128, seed=3)
+    rng = np.random.default_rng(0)
+    trace = []
+    for t in range(12):
+        u = t % 3
+        dn = int(rng.integers(20, 90))
+        trace.append({"ts": t, "user": u, "dn": dn, "nc": 4, "tokens": rng.integers(0, 128, dn).tolist(),
+                      "cands": rng.integers(0, 128, 4).tolist()})
+    eng = mtkv.Engine(_kv(kv), mode="hierarchical", backend="value", batch_size=3,
+                      model=mtkv.ModelConfig(**mc), keep_logits=True)
+    from oracle.oracle import Oracle
+    o = Oracle(kv, mode="hierarchical", batch_size=3, model=ModelParams(**mc))
+    worst = 0.0
+    for b in batches(trace, 3):
+        eng.process_batch(b)
+        o.process_batch(b)
+        assert eng.plans() == o.plans()
+        for g, r in zip(eng.last_logits(), o.logits()):
+            worst = max(worst, _rel_logit_err(g, r))
+    print("d=256 worst rel logit err", worst)
+    assert worst <= LOGIT_TOL
+
+
+def _paged_pool(L, P, S, d, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(L, P, 2, S, d, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("H,D,S,p_pre,n_q", [(2, 128, 32, 1000, 72), (4, 64, 16, 0, 130), (1, 32, 8, 333, 5),
+                                               (2, 16, 32, 4096, 64), (1, 8, 4, 17, 3)])
+def test_paged_attention_op_vs_torch_fp32(H, D, S, p_pre, n_q):
+    d, L = H * D, 2
+    n_keys = p_pre + n_q
+    P = (n_keys + S - 1) // S + 7
+    pool = _paged_pool(L, P, S, d, seed=H * 1000 + D)
+    pages = torch.randperm(P, device="cuda")[: (n_keys + S - 1) // S].to(torch.int32)
+    q = (torch.randn(n_q, d, device="cuda") * 0.5).to(torch.bfloat16)
+    out = torch.empty(n_q, d, device="cuda", dtype=torch.float32)
+    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=S, chunk_size=S, device_pages=P))
+    layer = 1
+    rc = mtkv.lib().mtkv_op_paged_attention(out.data_ptr(), q.data_ptr(), pool.data_ptr(), pages.data_ptr(),
+                                            n_q, p_pre, n_keys, layer, mtkv.C.byref(kv._c()), P,
+                                            torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, mtkv._err()
+    torch.cuda.synchronize()
+    K = pool[layer, pages.long(), 0].reshape(-1, d)[:n_keys].float()
+    V = pool[layer, pages.long(), 1].reshape(-1, d)[:n_keys].float()
+    qf = q.float()
+    ref = torch.empty_like(out)
+    pos_q = torch.arange(n_q, device="cuda") + p_pre
+    mask = torch.arange(n_keys, device="cuda")[None, :] <= pos_q[:, None]
+    for h in range(H):
+        s = qf[:, h * D:(h + 1) * D] @ K[:, h * D:(h + 1) * D].T / D ** 0.5
+        s = s.masked_fill(~mask, float("-inf"))
+        ref[:, h * D:(h + 1) * D] = torch.softmax(s, dim=-1) @ V[:, h * D:(h + 1) * D]
+    err = (out - ref).abs().max().item()
+    print(f"attention H={H} D={D} S={S} p_pre={p_pre} n_q={n_q}: max abs err {err:.2e}")
+    assert err <= ATTN_TOL
+
+
+def test_scatter_gather_round_trip_bit_exact():
+    L, H, D, S, chunk, P = 3, 2, 64, 32, 128, 40
+    d = H * D
+    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=S, chunk_size=chunk, device_pages=P))
+    n_chunks, ppc = 3, chunk // S
+    staging = torch.randint(-30000, 30000, (n_chunks, L, 2, chunk, d), dtype=torch.int16, device="cuda")
+    pool = torch.zeros(L, P, 2, S, d, dtype=torch.int16, device="cuda")
+    pages = torch.randperm(P, device="cuda")[: n_chunks * ppc].to(torch.int32)
+    s = torch.cuda.current_stream().cuda_stream
+    assert mtkv.lib().mtkv_op_scatter_chunks(pool.data_ptr(), staging.data_ptr(), pages.data_ptr(), n_chunks,
+                                             mtkv.C.byref(kv._c()), P, s) == 0
+    back = torch.zeros_like(staging)
+    assert mtkv.lib().mtkv_op_gather_chunks(back.data_ptr(), pool.data_ptr(), pages.data_ptr(), n_chunks,
+                                            mtkv.C.byref(kv._c()), P, s) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(back, staging)
+    # page p of chunk c holds tokens [p*S, (p+1)*S) of that chunk, every layer, K and V
+    pl = pages.long().view(n_chunks, ppc)
+    for c in range(n_chunks):
+        for p in range(ppc):
+            assert torch.equal(pool[:, pl[c, p]], staging[c, :, :, p * S:(p + 1) * S])
