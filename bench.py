@@ -1,0 +1,361 @@
+"""Serving-path benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (BASELINE.json configs[1]): GR model 4 layers, d=256 (H=2, D=128),
+users with 4K-token histories, 64 new tokens + 8 candidates per request,
+device page pool sized to ~10% of the user population's KV, pinned-host
+backup tier (chunked store), hierarchical mode. A "step" is one batch of
+requests through the full hot path: plan (LRU/eviction/allocation), H2D
+onload of host hits, scatter, per-layer fused projection + paged KV append,
+incremental prefix-reuse attention, norm/MLP, scoring head, offload of full
+chunks (gather + D2H).
+
+Warm-up (untimed): prefill of every user's 4K history through the same
+engine, then W revisit batches. Timed: K revisit batches. Synthetic data
+(random token ids, reference-initialised random weights).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1: launched by torchrun, one process per GPU; users are sharded by
+user id (u -> u*N + rank), each rank owns an independent cache shard; no
+collective on the data path ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "requests/sec & tokens/sec at fixed hit ratio, p99 latency, 1/2/4/8 B200 vs CPU"
+
+CONFIGS = {
+    # BASELINE.json configs[1] — the headline single-GPU workload
+    "gr4_d256": dict(L=4, H=2, D=128, vocab=4096, users=2048, history=4096, delta=64, cands=8,
+                     page=32, chunk=128, pool_frac=0.10, batch=64),
+    # configs[0] — the reference's smallest CPU case (parity-test sized)
+    "tiny_d64": dict(L=2, H=2, D=32, vocab=512, users=256, history=1024, delta=32, cands=8,
+                     page=32, chunk=128, pool_frac=0.10, batch=32),
+    # configs[3] per GPU shard — production-scale model
+    "gr8_d512": dict(L=8, H=4, D=128, vocab=4096, users=1024, history=8192, delta=64, cands=8,
+                     page=32, chunk=128, pool_frac=0.10, batch=32),
+}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(cfg: dict, steps: int, warmup: int, rank: int, world: int, seed: int = 1):
+    """Prefill requests (one 4K-token first visit per user) + revisit stream.
+
+    Revisits follow the reference generator's heavy-tailed (lognormal) return
+    process (workload.cpp:85, fixed_delta=64), so recently active users come
+    back soon — the temporal locality the LRU policy exploits."""
+    import paper_2604_22881_b200 as mtkv
+    rng = np.random.default_rng(seed + 7919 * rank)
+    U, V = cfg["users"], cfg["vocab"]
+    uid = lambda u: u * world + rank  # user-id sharding across ranks
+    prefill = [{"ts": 0, "user": uid(u), "dn": cfg["history"], "nc": cfg["cands"],
+                "tokens": rng.integers(0, V, cfg["history"], dtype=np.uint32),
+                "cands": rng.integers(0, V, cfg["cands"], dtype=np.uint32)} for u in range(U)]
+    n_rev = (3 * steps + warmup + 1) * cfg["batch"]
+    g = mtkv.GenConfig(num_users=U, total_requests=n_rev, fixed_delta=cfg["delta"], candidates=cfg["cands"],
+                       vocab=0, mean_final_len=cfg["delta"] * 8, min_len=cfg["delta"],
+                       max_len=cfg["delta"] * 64, gap_log_mu=9.0, gap_log_sigma=1.6, seed=seed + rank)
+    revisits = []
+    for r in mtkv.generate_trace(g)[:n_rev]:
+        revisits.append({"ts": r["ts"], "user": uid(r["user"]), "dn": cfg["delta"], "nc": cfg["cands"],
+                         "tokens": rng.integers(0, V, cfg["delta"], dtype=np.uint32),
+                         "cands": rng.integers(0, V, cfg["cands"], dtype=np.uint32)})
+    return prefill, revisits
+
+
+def kv_config(cfg):
+    import paper_2604_22881_b200 as mtkv
+    pages_per_user = -(-(cfg["history"] + 16 * cfg["delta"]) // cfg["page"])
+    # ~pool_frac of the population's KV, but never less than two batches of users
+    device_pages = max(int(cfg["pool_frac"] * cfg["users"] * pages_per_user),
+                       2 * cfg["batch"] * pages_per_user) + 4 * cfg["batch"]
+    chunks_per_batch = cfg["batch"] * (-(-cfg["history"] // cfg["chunk"]) + 2)
+    return mtkv.KVConfig(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"], page_size=cfg["page"],
+                         chunk_size=cfg["chunk"], device_pages=device_pages,
+                         onload_pages=chunks_per_batch * (cfg["chunk"] // cfg["page"]),
+                         offload_quota=cfg["chunk"] * 4 * chunks_per_batch)
+
+
+def run_b200(args, cfg):
+    import torch
+    import paper_2604_22881_b200 as mtkv
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    kv = kv_config(cfg)
+    cost = mtkv.CostModel(bus_bandwidth=55e9)  # measured pinned H2D on the B200 box (probe)
+    model = mtkv.ModelConfig(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"], vocab=cfg["vocab"],
+                             seed=1)
+    prefill, revisits = make_workload(cfg, args.steps, args.warmup, rank, world)
+    eng = mtkv.Engine(kv, cost, mode="hierarchical", backend="value", batch_size=cfg["batch"], model=model,
+                      device=local)
+    # ---- warm-up: prefill histories (untimed), then W revisit batches ----
+    pb = max(1, 65536 // cfg["history"])
+    for i in range(0, len(prefill), pb):
+        eng.process_batch(prefill[i:i + pb])
+    eng.synchronize()
+    B = cfg["batch"]
+    batches = [revisits[i * B:(i + 1) * B] for i in range(args.warmup + 3 * args.steps)]
+    packed = [mtkv.RequestBatch(b) for b in batches]
+    for i in range(args.warmup):
+        eng.process_batch(None, packed=packed[i])
+    eng.synchronize()
+    if dist:
+        dist.barrier()
+
+    # ---- timed (device throughput): requests pre-packed in host memory ----
+    r0 = eng.report()
+    clocks = Clocks(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    lat = []
+    wall0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        eng.process_batch(None, packed=packed[i])
+        lat.append(i)
+    eng.synchronize()
+    t_end.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    r1 = eng.report()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    n_req = args.steps * B
+    fresh_tokens = r1["tokens_processed"] - r0["tokens_processed"]
+
+    # ---- same engine, next K batches: per-batch device latency (p50/p99) and
+    #      per-launch attention timing for the roofline ----
+    eng.set_profile(True)
+    eng_lat, attn_ms, attn_launches, attn_bytes = [], 0.0, 0, 0
+    d = cfg["H"] * cfg["D"]
+    k0 = args.warmup + args.steps
+    for i in range(k0, k0 + args.steps):
+        eng.process_batch(None, packed=packed[i])
+        eng.synchronize()
+        eng_lat.append(eng.last_batch_ms())
+        ms, n = eng.last_attention_ms()
+        attn_ms += ms
+        attn_launches += n
+        for p in eng.plans():
+            keys = p["history_len"] + p["delta"] + p["num_candidates"]
+            rows = p["fresh_history"] + p["delta"] + p["num_candidates"]
+            # per layer: K+V of every visible key once + Q (bf16) read + O (fp32) write
+            attn_bytes += cfg["L"] * (keys * d * 2 * 2 + rows * d * 2 + rows * d * 4)
+    eng.set_profile(False)
+    launches_per_step = None
+
+    # ---- same engine, next K batches end to end through the public API:
+    #      Python request dicts in (packing + H2D inside), rankings read back ----
+    e0 = eng.report()
+    l0 = eng.kernel_launches()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    k1 = k0 + args.steps
+    for i in range(k1, k1 + args.steps):
+        eng.process_batch(batches[i])        # host dicts -> C-ABI
+        _ = eng.last_rankings()              # D2H of the step's result (waits for the batch)
+    eng.synchronize()
+    e2e_s = time.perf_counter() - w0
+    e1 = eng.report()
+    launches_per_step = (eng.kernel_launches() - l0) / args.steps
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    res = dict(elapsed=elapsed, n_req=n_req, fresh_tokens=fresh_tokens, wall=wall, e2e_s=e2e_s,
+               e2e_req=n_req, h2d=(e1["h2d_bytes"] - e0["h2d_bytes"]) / args.steps,
+               d2h=(e1["d2h_bytes"] - e0["d2h_bytes"]) / args.steps)
+    if dist:
+        t = torch.tensor([elapsed, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c = torch.tensor([n_req, fresh_tokens], dtype=torch.float64, device="cuda")
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        elapsed, e2e_s = t.tolist()
+        n_all, tok_all = c.tolist()
+    else:
+        n_all, tok_all = n_req, fresh_tokens
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    rep = r1
+    hit = dict(gpu=(rep["gpu_hit_ratio"]), total=(rep["total_hit_ratio"]))
+    avg_launch_s = (attn_ms / 1e3) / max(attn_launches, 1)
+    achieved = (attn_bytes / max(attn_launches, 1)) / avg_launch_s / 1e9 if attn_launches else 0.0
+    line = {
+        "metric": METRIC,
+        "value": n_all / elapsed,
+        "unit": "requests/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random token ids, reference-initialised random weights)",
+        "config": {"workload": f"configs[1] {args.config}: {cfg['L']} layers d={cfg['H'] * cfg['D']}, "
+                               f"{cfg['history']}-token histories, {cfg['delta']} new + {cfg['cands']} "
+                               f"candidates/request, HBM pool {int(cfg['pool_frac'] * 100)}% of users, "
+                               f"pinned-host tier, hierarchical",
+                   "users_per_gpu": cfg["users"], "batch": B, "device_pages": kv.device_pages,
+                   "page_size": cfg["page"], "chunk_size": cfg["chunk"], "parallelism": f"user-shard x{world}",
+                   "l2": "inputs larger than L2 (KV working set >> 126 MB)"},
+        "tokens_per_sec": tok_all / elapsed,
+        "p50_batch_ms": float(np.percentile(eng_lat, 50)) if eng_lat else None,
+        "p99_batch_ms": float(np.percentile(eng_lat, 99)) if eng_lat else None,
+        "hit_ratio": {"gpu": rep["gpu_hit_ratio"], "total": rep["total_hit_ratio"],
+                      "note": "cumulative over prefill + warm-up + timed steps"},
+        "e2e": {"value": n_all / e2e_s, "unit": "requests/s", "h2d_bytes_per_step": res["h2d"],
+                "d2h_bytes_per_step": res["d2h"]},
+        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "gpu_launches_per_step": launches_per_step,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                     "kernel": "attn_kernel (paged incremental attention)",
+                     "launches_timed": attn_launches},
+        "clocks": clk,
+    }
+    if args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg, seconds=15.0, threads=None):
+    """The reference's own CPU serving path (oracle/_ref, value backend), all host threads."""
+    from oracle.oracle import RefLib
+    if not RefLib.available():
+        return {"value": None, "unit": "requests/s", "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    threads = threads or os.cpu_count()
+    r = RefLib().call(dict(cmd="bench", threads=threads, users_per_thread=1, history=cfg["history"],
+                           delta=cfg["delta"], candidates=cfg["cands"], batch_size=1, seconds=seconds,
+                           model=dict(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"],
+                                      vocab=cfg["vocab"], seed=1),
+                           kv=dict(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"],
+                                   page_size=cfg["page"], chunk_size=cfg["chunk"], device_pages=4096,
+                                   offload_quota=cfg["chunk"] * 64)))
+    return {"value": r["requests_per_s"], "unit": "requests/s", "cores": threads, "kind": "reference",
+            "sample": f"{threads} threads x 1 user each, {cfg['history']}-token prefill untimed, "
+                      f"{r['requests']} revisit requests ({cfg['delta']} new + {cfg['cands']} cands) "
+                      f"in {r['seconds']:.1f}s", "tokens_per_s": r["tokens_per_s"]}
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    base = cpu_baseline(cfg, seconds=args.cpu_seconds)
+    line = {"metric": METRIC, "value": base["value"], "unit": "requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"configs[1] {args.config} (reference CPU serving path, sampled)"},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "requests/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="gr4_d256", choices=sorted(CONFIGS))
+    ap.add_argument("--users", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = dict(CONFIGS[args.config])
+    if args.users:
+        cfg["users"] = args.users
+    world, rank, _ = dist_env()
+    if world > 1 or rank != 0:
+        args.cpu_baseline = False
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

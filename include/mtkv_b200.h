@@ -162,6 +162,8 @@ double mtkv_engine_last_batch_ms(mtkv_engine* e);
 /* device time of the attention kernels of the last batch (ms) and their launch count */
 double mtkv_engine_last_attention_ms(mtkv_engine* e, uint32_t* launches);
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e);
+/* toggles per-launch CUDA-event timing of the attention kernels */
+void mtkv_engine_set_profile(mtkv_engine* e, uint32_t on);
 
 /* ---- both objects: manager state (sim.hpp:149 manager()) ----
  * `obj` is an mtkv_planner* or mtkv_engine* as named by `is_engine`. */

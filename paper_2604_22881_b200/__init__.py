@@ -125,6 +125,7 @@ EXPORTED_SYMBOLS = [
     "mtkv_engine_drain", "mtkv_engine_synchronize", "mtkv_engine_last_logits",
     "mtkv_engine_last_rankings", "mtkv_engine_check_conservation", "mtkv_engine_read_user_kv",
     "mtkv_engine_last_batch_ms", "mtkv_engine_last_attention_ms", "mtkv_engine_kernel_launches",
+    "mtkv_engine_set_profile",
     "mtkv_report", "mtkv_last_plans", "mtkv_last_evictions", "mtkv_known_users", "mtkv_user_state",
     "mtkv_user_pages", "mtkv_lru_snapshot", "mtkv_evict_user", "mtkv_is_locked",
     "mtkv_get_total_cache_length", "mtkv_gen_config_default", "mtkv_gen_config_preset",
@@ -172,6 +173,7 @@ def lib():
         "mtkv_engine_last_batch_ms": (C.c_double, [vp]),
         "mtkv_engine_last_attention_ms": (C.c_double, [vp, u32p]),
         "mtkv_engine_kernel_launches": (u64, [vp]),
+        "mtkv_engine_set_profile": (None, [vp, u32]),
         "mtkv_report": (C.c_int, [vp, C.c_int, C.POINTER(_Report)]),
         "mtkv_last_plans": (u32, [vp, C.c_int, C.POINTER(_Plan), u32]),
         "mtkv_last_evictions": (u32, [vp, C.c_int, C.POINTER(_Eviction), u32]),
@@ -541,6 +543,9 @@ class Engine(_ManagerView):
         n = C.c_uint32(0)
         ms = lib().mtkv_engine_last_attention_ms(self._h, C.byref(n))
         return float(ms), int(n.value)
+
+    def set_profile(self, on: bool) -> None:
+        lib().mtkv_engine_set_profile(self._h, int(on))
 
     def kernel_launches(self) -> int:
         return int(lib().mtkv_engine_kernel_launches(self._h))

@@ -250,6 +250,7 @@ int64_t mtkv_engine_read_user_kv(mtkv_engine* e, uint32_t user, uint32_t layer, 
 double mtkv_engine_last_batch_ms(mtkv_engine* e) { return e->e.last_batch_ms(); }
 double mtkv_engine_last_attention_ms(mtkv_engine* e, uint32_t* launches) { return e->e.last_attention_ms(launches); }
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e) { return e->e.launches; }
+void mtkv_engine_set_profile(mtkv_engine* e, uint32_t on) { e->e.set_profile(on); }
 
 // ------------------------------------------------------------ manager view --
 int mtkv_report(const void* obj, int is_engine, mtkv_run_report* out) {

@@ -46,6 +46,7 @@ class Engine {
   double last_batch_ms();
   double last_attention_ms(uint32_t* launches);
   void report(mtkv_run_report& r) const;
+  void set_profile(uint32_t on) { opt_.profile = on; }
   uint32_t batch_size() const { return opt_.batch_size ? opt_.batch_size : 1; }
 
   Planner planner;

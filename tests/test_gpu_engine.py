@@ -6,7 +6,8 @@ Bars (stated here, as DESIGN.md §(c)):
   * data movement (tag backend): bit-exact — every byte of every resident
     token on device and of every persisted host chunk is checked;
   * numerics (value backend, bf16 storage / fp32 accumulate vs fp64 reference):
-    per request max|dlogit| <= LOGIT_TOL * max(1, max|logit|); K/V max abs
+    per request max|dlogit| <= LOGIT_TOL * max|logit| (row scale) and the mean of
+    that ratio over all requests <= LOGIT_MEAN_TOL; K/V max abs
     error <= KV_TOL * max|kv|; attention op vs torch fp32 <= ATTN_TOL abs.
 """
 import numpy as np
@@ -19,7 +20,8 @@ from tests.util import REPORT_KEYS, batches, golden_cases, state_digest
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_TOL = 0.05
+LOGIT_TOL = 0.08
+LOGIT_MEAN_TOL = 0.02
 KV_TOL = 0.03
 ATTN_TOL = 2e-2
 
@@ -57,8 +59,10 @@ def test_tag_engine_bit_exact(case):
 
 
 def _rel_logit_err(a, b):
+    """max|a-b| relative to the row's logit scale (the reference model has no
+    residual path, so logits are tiny, ~1e-8; bf16 keeps relative precision)."""
     a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
-    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
 
 
 @pytest.mark.parametrize("case", golden_cases("value"), ids=lambda c: c["name"])
@@ -75,9 +79,10 @@ def test_value_engine_logits_match_reference(case):
         ref = np.array(run["logits"])
         got = np.array(got)
         assert got.shape == ref.shape
-        worst = max(_rel_logit_err(g, r) for g, r in zip(got, ref))
-        print(f"{case['name']} {run['mode']} bs{run['batch_size']}: worst rel logit err {worst:.3e}")
-        assert worst <= LOGIT_TOL
+        errs = [_rel_logit_err(g, r) for g, r in zip(got, ref)]
+        worst, mean = max(errs), float(np.mean(errs))
+        print(f"{case['name']} {run['mode']} bs{run['batch_size']}: rel logit err max {worst:.3e} mean {mean:.3e}")
+        assert worst <= LOGIT_TOL and mean <= LOGIT_MEAN_TOL
 
 
 def test_value_engine_kv_matches_oracle():
@@ -121,9 +126,10 @@ def test_value_engine_rankings():
         ranked = eng.last_rankings()[0]
         ref_logits = run["logits"][i]
         want = mtkv.rank_candidates(ref_logits, b[0]["cands"])
+        scale = max(abs(x) for x in ref_logits)
         margin = min((abs(ref_logits[x] - ref_logits[y]) for x in b[0]["cands"] for y in b[0]["cands"]
-                      if x != y and ref_logits[x] != ref_logits[y]), default=1.0)
-        if margin > 0.05:  # orderings decided by more than the bf16 error bar must agree exactly
+                      if x != y and ref_logits[x] != ref_logits[y]), default=scale)
+        if margin > 0.05 * scale:  # orderings decided by more than the bf16 error bar must agree exactly
             total += 1
             agree += ranked == want
     assert total > 0 and agree == total
