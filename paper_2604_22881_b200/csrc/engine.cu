@@ -67,6 +67,14 @@ Engine::Engine(const mtkv_kv_config& kv, const mtkv_cost_model& cost, const mtkv
 }
 
 Engine::~Engine() {
+  if (refill_.joinable()) {
+    {
+      std::lock_guard<std::mutex> g(slab_mu_);
+      stop_refill_ = true;
+    }
+    slab_cv_.notify_all();
+    refill_.join();
+  }
   if (comp_) cudaDeviceSynchronize();
   DevBuf* bufs[] = {&pool_, &staging_[0], &staging_[1], &offload_, &meta_, &x_, &x2_, &u_, &q_,
                     &mid_, &part_o_, &part_lse_, &logits_, &scores_};
@@ -181,28 +189,90 @@ int Engine::init(std::string& err) {
     for (uint64_t s = slots; s-- > 0;) off_free_.push_back(uint32_t(s));
     off_slot_batch_.assign(slots, -1);
   }
-  slab_bytes_ = std::max<size_t>(size_t(256) << 20, chunk_bytes_ * 8);
-  slab_used_ = slab_bytes_;  // force a slab on first use
+  // host extents of ~8 MB (>= 1 chunk) and slabs of >= 4 extents
+  chunks_per_extent_ = uint32_t(std::max<size_t>(1, (size_t(8) << 20) / chunk_bytes_));
+  slab_bytes_ = std::max<size_t>(size_t(256) << 20, chunk_bytes_ * chunks_per_extent_ * 4);
+  if (opt_.mode == MTKV_MODE_HIERARCHICAL) refill_ = std::thread([this] { slab_refill_loop(); });
+  // staging for the largest onload a batch may plan (KVConfig::onload_pages),
+  // allocated up front so no timed batch reallocates (capped; grows lazily past it)
+  if (opt_.mode == MTKV_MODE_HIERARCHICAL) {
+    const size_t slots = size_t(kv_.onload_pages) * kv_.page_size / kv_.chunk_size;
+    const size_t bytes = std::min(slots * chunk_bytes_, size_t(8) << 30);
+    if (bytes && (staging_[0].ensure(bytes) || staging_[1].ensure(bytes))) {
+      err = "engine: cannot allocate the onload staging buffers";
+      return MTKV_ERROR;
+    }
+  }
   if (value_) init_weights();
   CK(cudaGetLastError());
   return MTKV_OK;
 }
 
-int Engine::host_chunk(uint64_t id, std::string& err) {
+// Pinned host store. A user's chunks live in per-user extents of
+// chunks_per_extent_ consecutive chunks, so the onload of a user's persisted
+// prefix is a handful of large copy-engine transfers instead of one per chunk.
+// Extents are carved from pinned slabs; a background thread keeps spare slabs
+// ready so cudaHostAlloc never lands on the serving path.
+char* Engine::take_slab() {
+  {
+    std::lock_guard<std::mutex> g(slab_mu_);
+    if (!spare_slabs_.empty()) {
+      char* s = spare_slabs_.back();
+      spare_slabs_.pop_back();
+      slab_cv_.notify_one();
+      return s;
+    }
+  }
+  char* s = nullptr;
+  if (cudaHostAlloc((void**)&s, slab_bytes_, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(slab_mu_);
+  slabs_.push_back(s);
+  slab_cv_.notify_one();
+  return s;
+}
+
+void Engine::slab_refill_loop() {
+  cudaSetDevice(opt_.device);
+  std::unique_lock<std::mutex> lk(slab_mu_);
+  while (!stop_refill_) {
+    if (spare_slabs_.size() < kSpareSlabs) {
+      lk.unlock();
+      char* s = nullptr;
+      const bool ok = cudaHostAlloc((void**)&s, slab_bytes_, cudaHostAllocDefault) == cudaSuccess;
+      lk.lock();
+      if (!ok) break;
+      slabs_.push_back(s);
+      spare_slabs_.push_back(s);
+      continue;
+    }
+    slab_cv_.wait(lk, [&] { return stop_refill_ || spare_slabs_.size() < kSpareSlabs; });
+  }
+}
+
+int Engine::host_chunk(uint64_t id, uint32_t user, uint32_t index, std::string& err) {
   if (id < chunk_ptr_.size() && chunk_ptr_[id]) return MTKV_OK;
-  if (slab_used_ + chunk_bytes_ > slab_bytes_) {
-    char* s = nullptr;
-    CK(cudaHostAlloc((void**)&s, slab_bytes_, cudaHostAllocDefault));
-    slabs_.push_back(s);
-    slab_used_ = 0;
+  std::vector<char*>& ext = user_extents_[user];
+  const uint32_t e = index / chunks_per_extent_;
+  while (ext.size() <= e) {
+    const size_t eb = chunk_bytes_ * chunks_per_extent_;
+    if (!cur_slab_ || slab_used_ + eb > slab_bytes_) {
+      cur_slab_ = take_slab();
+      slab_used_ = 0;
+      if (!cur_slab_) {
+        err = "engine: pinned host allocation failed";
+        return MTKV_ERROR;
+      }
+    }
+    ext.push_back(cur_slab_ + slab_used_);
+    slab_used_ += eb;
   }
   if (chunk_ptr_.size() <= id) {
-    chunk_ptr_.resize(id + 1, nullptr);
-    chunk_d2h_batch_.resize(id + 1, -1);
-    chunk_off_slot_.resize(id + 1, -1);
+    const size_t n = std::max<size_t>(id + 1, chunk_ptr_.size() * 2);
+    chunk_ptr_.resize(n, nullptr);
+    chunk_d2h_batch_.resize(n, -1);
+    chunk_off_slot_.resize(n, -1);
   }
-  chunk_ptr_[id] = slabs_.back() + slab_used_;
-  slab_used_ += chunk_bytes_;
+  chunk_ptr_[id] = ext[e] + size_t(index % chunks_per_extent_) * chunk_bytes_;
   return MTKV_OK;
 }
 
@@ -271,6 +341,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   std::vector<ReqDev> rd(n);
   uint32_t rows = 0, part_rows = 0, max_hist = 0, n_items = 0, ncand_total = 0;
   constexpr uint32_t kSplitKeys = 512;
+  uint32_t max_q = 0;
+  for (uint32_t r = 0; r < n; ++r)
+    max_q = std::max(max_q, w.reqs[r].n_hist + w.reqs[r].plan.num_candidates);
+  const uint32_t bq = max_q > 64 ? 128 : 64;  // one tile covers typical fresh rows (Δ + candidates)
   for (uint32_t r = 0; r < n; ++r) {
     const ReqWork& R = w.reqs[r];
     ReqDev& x = rd[r];
@@ -285,11 +359,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     x.n_scratch = recompute_ ? t_ns[r] : R.n_scratch;
     x.user = R.plan.user;
     const uint64_t T = x.start + x.n_q;
-    x.split_keys = x.n_q <= 128 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 64, 0xFFFFFFFFull));
+    x.split_keys = x.n_q <= 256 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 64, 0xFFFFFFFFull));
     x.n_splits = uint32_t((T + x.split_keys - 1) / x.split_keys);
     x.part_base = part_rows;
     part_rows += x.n_splits * x.n_q;
-    const uint32_t bq = 64;
     n_items += H * ((x.n_q + bq - 1) / bq) * x.n_splits;
     rows += x.n_q;
     ncand_total += x.n_cand;
@@ -363,7 +436,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     }
     h_last[r] = x.q_row0 + x.n_q - 1;
     for (uint32_t h = 0; h < H; ++h)
-      for (uint32_t qt = 0; qt < (x.n_q + 63) / 64; ++qt)
+      for (uint32_t qt = 0; qt < (x.n_q + bq - 1) / bq; ++qt)
         for (uint32_t s = 0; s < x.n_splits; ++s) h_items[it++] = AttnItem{r, h, qt, s};
     last_nc_[r] = x.n_cand;
     for (uint32_t c = 0; c < x.n_cand; ++c) {
@@ -386,24 +459,37 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   // ---- onload: copy-engine H2D into staging[batch % 2] ----
   const int sb = int(batch_no_ % 2);
   if (n_on) {
-    if (staging_slots_ < n_on || !staging_[sb].p || staging_[sb].bytes < size_t(n_on) * chunk_bytes_) {
-      if (staging_[sb].ensure(size_t(n_on) * chunk_bytes_)) { err = "engine: staging alloc"; return MTKV_ERROR; }
+    if (staging_[sb].bytes < size_t(n_on) * chunk_bytes_ &&
+        staging_[sb].ensure(size_t(n_on) * chunk_bytes_)) {
+      err = "engine: staging alloc";
+      return MTKV_ERROR;
     }
     if (batch_no_ >= 2) CK(cudaStreamWaitEvent(h2d_, ev_scatter_[(batch_no_ - 2) % kRing], 0));
     int64_t waited = -1;
-    for (uint32_t j = 0; j < n_on; ++j) {
+    for (uint32_t j = 0; j < n_on;) {
+      // a run of chunks contiguous in the host extent -> one transfer into
+      // consecutive staging slots
+      uint32_t run = 1;
       const ChunkMove& m = w.onloads[j];
       if (m.chunk_id >= chunk_ptr_.size() || !chunk_ptr_[m.chunk_id]) {
         err = "engine: onload of a chunk with no host copy";
         return MTKV_ERROR;
       }
-      const int64_t b = chunk_d2h_batch_[m.chunk_id];
+      int64_t b = chunk_d2h_batch_[m.chunk_id];
+      while (j + run < n_on) {
+        const ChunkMove& nx = w.onloads[j + run];
+        if (nx.chunk_id >= chunk_ptr_.size() || chunk_ptr_[nx.chunk_id] != chunk_ptr_[m.chunk_id] + run * chunk_bytes_)
+          break;
+        b = std::max(b, chunk_d2h_batch_[nx.chunk_id]);
+        ++run;
+      }
       if (b >= 0 && b > waited) {
         CK(cudaStreamWaitEvent(h2d_, ev_d2h_[b % kRing], 0));
         waited = b;
       }
       CK(cudaMemcpyAsync(static_cast<char*>(staging_[sb].p) + size_t(j) * chunk_bytes_, chunk_ptr_[m.chunk_id],
-                         chunk_bytes_, cudaMemcpyHostToDevice, h2d_));
+                         size_t(run) * chunk_bytes_, cudaMemcpyHostToDevice, h2d_));
+      j += run;
     }
     CK(cudaEventRecord(ev_onload_[k], h2d_));
     h2d_bytes_ += uint64_t(n_on) * chunk_bytes_;
@@ -467,7 +553,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       AttnArgs aa{};
       aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.items = d_items; aa.n_items = n_items;
       aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
-      aa.g = g_; aa.layer = l; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
+      aa.g = g_; aa.layer = l; aa.bq = bq; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
       launch_attention(aa, comp_);
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l + 1], comp_));
@@ -531,7 +617,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     CK(cudaStreamWaitEvent(d2h_, ev_gathered_[k], 0));
     for (uint32_t j = 0; j < n_off; ++j) {
       const ChunkMove& m = w.offloads[j];
-      if (host_chunk(m.chunk_id, err)) return MTKV_ERROR;
+      if (host_chunk(m.chunk_id, m.user, m.chunk_index, err)) return MTKV_ERROR;
       CK(cudaMemcpyAsync(chunk_ptr_[m.chunk_id], static_cast<char*>(offload_.p) + size_t(off_slots[j]) * chunk_bytes_,
                          chunk_bytes_, cudaMemcpyDeviceToHost, d2h_));
       chunk_d2h_batch_[m.chunk_id] = int64_t(batch_no_);

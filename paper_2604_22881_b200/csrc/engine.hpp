@@ -12,7 +12,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <condition_variable>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "kernels.cuh"
@@ -54,7 +58,9 @@ class Engine {
 
  private:
   int enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, std::string& err);
-  int host_chunk(uint64_t id, std::string& err);  // ensure pinned storage for chunk id
+  int host_chunk(uint64_t id, uint32_t user, uint32_t index, std::string& err);  // pinned storage
+  char* take_slab();
+  void slab_refill_loop();
   void init_weights();
 
   mtkv_kv_config kv_;
@@ -80,9 +86,17 @@ class Engine {
   float* w_ln_ = nullptr;
   uint32_t staging_slots_ = 0;
 
-  // pinned host memory
-  std::vector<char*> slabs_;
+  // pinned host memory: slabs -> per-user extents -> chunks
+  static constexpr size_t kSpareSlabs = 2;
+  std::vector<char*> slabs_, spare_slabs_;
+  std::mutex slab_mu_;
+  std::condition_variable slab_cv_;
+  std::thread refill_;
+  bool stop_refill_ = false;
+  char* cur_slab_ = nullptr;
   size_t slab_bytes_ = 0, slab_used_ = 0;
+  uint32_t chunks_per_extent_ = 1;
+  std::unordered_map<uint32_t, std::vector<char*>> user_extents_;
   std::vector<char*> chunk_ptr_;          // chunk id -> pinned [L][2][chunk][d]
   std::vector<int64_t> chunk_d2h_batch_;  // batch whose d2h ring event covers the chunk
   std::vector<uint32_t> off_free_;        // free offload slots

@@ -212,7 +212,7 @@ void launch_embed(__nv_bfloat16* x, const __nv_bfloat16* table, const uint32_t* 
 // Keys stream page by page through a 2-stage cp.async ring (64 keys/stage).
 // Key index == position: indices [0, start+n_hist) live in the user's pages,
 // [start+n_hist, start+n_hist+n_cand) in the request's scratch pages.
-constexpr int ABQ = 64, ABK = 64;
+constexpr int ABK = 64;
 
 __device__ __forceinline__ const __nv_bfloat16* key_row(const AttnArgs& a, const ReqDev& R, uint64_t idx,
                                                         uint32_t kv, uint32_t h) {
@@ -229,7 +229,7 @@ __device__ __forceinline__ const __nv_bfloat16* key_row(const AttnArgs& a, const
   return a.pool + a.g.off(a.layer, page, kv, slot) + (size_t)h * a.g.D;
 }
 
-template <int DP, bool VEC>
+template <int DP, bool VEC, int NT>
 __device__ __forceinline__ void attn_load_kv(const AttnArgs& a, const ReqDev& R, __nv_bfloat16* Ks,
                                              __nv_bfloat16* Vs, uint64_t k0, uint64_t k_hi, uint32_t h,
                                              int tid) {
@@ -237,7 +237,7 @@ __device__ __forceinline__ void attn_load_kv(const AttnArgs& a, const ReqDev& R,
   const uint32_t D = a.g.D;
   if constexpr (VEC) {
     const int live = (int)((D + 7) / 8);
-    for (int c = tid; c < ABK * CH; c += 128) {
+    for (int c = tid; c < ABK * CH; c += NT) {
       const int row = c / CH, ch = c % CH;
       if (ch >= live) continue;
       const uint64_t idx = k0 + row;
@@ -248,7 +248,7 @@ __device__ __forceinline__ void attn_load_kv(const AttnArgs& a, const ReqDev& R,
       cp_async16(Vs + row * LD + ch * 8, vr + (ok ? ch * 8 : 0), ok);
     }
   } else {
-    for (int c = tid; c < ABK * (int)D; c += 128) {
+    for (int c = tid; c < ABK * (int)D; c += NT) {
       const int row = c / D, j = c % D;
       const uint64_t idx = k0 + row;
       __nv_bfloat16 kv0 = __float2bfloat16(0.f), kv1 = __float2bfloat16(0.f);
@@ -263,9 +263,11 @@ __device__ __forceinline__ void attn_load_kv(const AttnArgs& a, const ReqDev& R,
   }
 }
 
-template <int DP, bool VEC>
-__global__ void __launch_bounds__(128) attn_kernel(AttnArgs a) {
-  constexpr int LD = DP + 8, NKT = ABK / 8, NDT = DP / 8;
+// NW warps x 16 query rows = one query tile; K/V of the split are streamed once
+// per tile, so a request whose fresh rows fit one tile reads its prefix once.
+template <int DP, bool VEC, int NW>
+__global__ void __launch_bounds__(NW * 32) attn_kernel(AttnArgs a) {
+  constexpr int LD = DP + 8, NKT = ABK / 8, NDT = DP / 8, NT = NW * 32, ABQ = NW * 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* Kb = Qs + ABQ * LD;
@@ -284,17 +286,17 @@ __global__ void __launch_bounds__(128) attn_kernel(AttnArgs a) {
   const uint64_t k_hi = min(k_vis, k_lo + (uint64_t)R.split_keys);
 
   // zero everything once: pad columns and masked rows stay finite
-  for (int i = tid; i < (ABQ + 4 * ABK) * LD / 8; i += 128)
+  for (int i = tid; i < (ABQ + 4 * ABK) * LD / 8; i += NT)
     reinterpret_cast<uint4*>(smem_raw)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   // Q tile
-  for (int c = tid; c < ABQ * (int)D; c += 128) {
+  for (int c = tid; c < ABQ * (int)D; c += NT) {
     const int row = c / D, j = c % D;
     if (q0 + row < q_end) Qs[row * LD + j] = a.q[(size_t)(R.q_row0 + q0 + row) * d + h * D + j];
   }
   const int n_tiles = k_hi > k_lo ? (int)((k_hi - k_lo + ABK - 1) / ABK) : 0;
   if (n_tiles > 0) {
-    attn_load_kv<DP, VEC>(a, R, Kb, Vb, k_lo, k_hi, h, tid);
+    attn_load_kv<DP, VEC, NT>(a, R, Kb, Vb, k_lo, k_hi, h, tid);
     cp_commit();
   }
   __syncthreads();
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(128) attn_kernel(AttnArgs a) {
     const int buf = t & 1;
     const uint64_t kbase = k_lo + (uint64_t)t * ABK;
     if (t + 1 < n_tiles) {
-      attn_load_kv<DP, VEC>(a, R, Kb + (buf ^ 1) * ABK * LD, Vb + (buf ^ 1) * ABK * LD, kbase + ABK, k_hi, h, tid);
+      attn_load_kv<DP, VEC, NT>(a, R, Kb + (buf ^ 1) * ABK * LD, Vb + (buf ^ 1) * ABK * LD, kbase + ABK, k_hi, h, tid);
       cp_commit();
       cp_wait<1>();
     } else {
@@ -420,18 +422,24 @@ __global__ void __launch_bounds__(128) attn_kernel(AttnArgs a) {
   }
 }
 
+template <int DP, bool VEC, int NW>
+static void launch_attn_cfg(const AttnArgs& a, cudaStream_t s) {
+  const size_t smem = (size_t)(NW * 16 + 4 * ABK) * (DP + 8) * sizeof(__nv_bfloat16);
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_kernel<DP, VEC, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = true;
+  }
+  attn_kernel<DP, VEC, NW><<<a.n_items, NW * 32, smem, s>>>(a);
+}
+
 template <int DP>
 static void launch_attn_dp(const AttnArgs& a, cudaStream_t s) {
-  const size_t smem = (size_t)(ABQ + 4 * ABK) * (DP + 8) * sizeof(__nv_bfloat16);
   const bool vec = (a.g.D % 8 == 0);
-  if (vec) {
-    static bool set = false;
-    if (!set) { cudaFuncSetAttribute(attn_kernel<DP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); set = true; }
-    attn_kernel<DP, true><<<a.n_items, 128, smem, s>>>(a);
+  if (a.bq == 128) {
+    if (vec) launch_attn_cfg<DP, true, 8>(a, s); else launch_attn_cfg<DP, false, 8>(a, s);
   } else {
-    static bool set = false;
-    if (!set) { cudaFuncSetAttribute(attn_kernel<DP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); set = true; }
-    attn_kernel<DP, false><<<a.n_items, 128, smem, s>>>(a);
+    if (vec) launch_attn_cfg<DP, true, 4>(a, s); else launch_attn_cfg<DP, false, 4>(a, s);
   }
 }
 

@@ -82,6 +82,7 @@ struct AttnArgs {
   PoolGeom g;
   uint32_t layer;
   float scale_log2;         // log2(e) / sqrt(D)
+  uint32_t bq;              // query rows per tile: 64 or 128 (items enumerate tiles of bq)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 

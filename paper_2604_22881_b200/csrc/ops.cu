@@ -89,7 +89,8 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   r.part_base = 0;
   r.n_splits = 1;
   r.split_keys = 0xFFFFFFFFu;
-  const uint32_t qtiles = (n_q + 63) / 64, n_items = g.H * qtiles;
+  const uint32_t bq = n_q > 64 ? 128 : 64;
+  const uint32_t qtiles = (n_q + bq - 1) / bq, n_items = g.H * qtiles;
   AttnItem* hi = new AttnItem[n_items];
   uint32_t k = 0;
   for (uint32_t h = 0; h < g.H; ++h)
@@ -116,6 +117,7 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   a.part_lse = lse;
   a.g = g;
   a.layer = layer;
+  a.bq = bq;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
   if (e == cudaSuccess) launch_attention(a, s);
   cudaFreeAsync(buf, s);
