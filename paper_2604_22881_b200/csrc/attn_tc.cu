@@ -1,0 +1,441 @@
+// Incremental prefix-reuse attention on the 5th-gen tensor cores (sm_100a).
+//
+// One CTA = (request, head, 128-row query tile, key split). Warp roles:
+//   warp 0      TMA producer: page-granular cp.async.bulk.tensor loads of K and V
+//               straight out of the paged pool (no gather pass), 2-stage ring
+//   warp 1      MMA issuer (one elected thread): S = Q K^T and O += P V with
+//               tcgen05.mma kind::f16, accumulators in TMEM
+//   warp 2      TMEM allocator (512 columns: S double buffer + O)
+//   warps 4..7  softmax warpgroup: thread r owns query row r; tcgen05.ld of its
+//               S row, mask, online softmax (base 2), P -> smem (bf16, SW128),
+//               conditional O rescale in TMEM, epilogue O/l + lse to HBM
+// Logical key space: the user's keys [0, KA) padded to a page boundary, then
+// the request's candidate keys (their own scratch pages), so every page-sized
+// slice of a tile is one TMA box. Keys past the end load as zeros (TMA OOB).
+//
+// Operand layouts (canonical UMMA, 128-byte swizzle, 1024-B aligned):
+//   Q, P, K : K-major  [rows][64-elem blocks], SBO = 1024 B, +32 B per K=16 step
+//   V       : MN-major [keys][64-dim blocks],  SBO = 1024 B, LBO = 16 KB
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace mtkv_b200 {
+
+namespace tc {
+
+constexpr int BM = 128;   // query rows per tile (TMEM lanes)
+constexpr int BN = 128;   // keys per tile
+constexpr int STAGES = 2;
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          s32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SW128 K-major / MN-major smem descriptor (sm_100: version 1, layout 2 = SWIZZLE_128B)
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// byte offset of 16-byte chunk `c` (of 8) in row `r` of a SW128 K-major block
+__device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct Smem {
+  static constexpr uint32_t kBlock = BM * 128;  // one 128-row x 64-elem bf16 block = 16 KB
+};
+
+}  // namespace tc
+
+using namespace tc;
+
+template <int D>
+__global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, AttnArgs a) {
+  constexpr int NB = D / 64;                      // 64-element column blocks of Q/K/V
+  constexpr uint32_t Q_BYTES = NB * Smem::kBlock;  // 128 rows x D
+  constexpr uint32_t P_BYTES = 2 * Smem::kBlock;   // 128 rows x 128 keys
+  constexpr uint32_t KV_BYTES = NB * Smem::kBlock; // 128 keys x D (K or V)
+  constexpr uint32_t STAGE_BYTES = 2 * KV_BYTES;
+  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t S_COL0 = 0, O_COL = 2 * BN;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sP = sQ + Q_BYTES;
+  uint8_t* sKV = sP + P_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;              // [STAGES]
+  uint64_t* empty = bars + STAGES;    // [STAGES]
+  uint64_t* s_full = bars + 2 * STAGES;      // [2]
+  uint64_t* s_free = s_full + 2;             // [2]
+  uint64_t* p_full = s_free + 2;
+  uint64_t* o_done = p_full + 1;
+  uint64_t* q_full = o_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+
+  const AttnItem it = a.items[blockIdx.x];
+  const ReqDev R = a.reqs[it.req];
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const PoolGeom& g = a.g;
+  const uint32_t S = g.S, h = it.head;
+
+  // logical key space: user keys [0, KA) padded to KAp, then candidates
+  const uint64_t KA = R.start + R.n_hist;
+  const uint64_t KAp = (KA + S - 1) / S * S;
+  const uint32_t user_pages = uint32_t(KAp / S);
+  const uint32_t q0 = it.qtile * BM;
+  const uint32_t q_end = min(R.n_q, q0 + BM);
+  const uint64_t pos_last = R.start + q_end - 1;
+  const uint64_t k_vis = pos_last >= KA ? KAp + (pos_last - KA + 1) : pos_last + 1;
+  const uint64_t k_lo = uint64_t(it.split) * R.split_keys;
+  const uint64_t k_hi = min(k_vis, k_lo + uint64_t(R.split_keys));
+  const int n_tiles = k_hi > k_lo ? int((k_hi - k_lo + BN - 1) / BN) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
+    mbar_init(q_full, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0 && n_tiles > 0) {
+      const int ppt = BN / S;  // pages per tile
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % STAGES;
+        if (t >= STAGES) mbar_wait(&empty[st], ((t / STAGES) - 1) & 1);
+        mbar_expect_tx(&full[st], STAGE_BYTES);
+        uint8_t* kdst = sKV + st * STAGE_BYTES;
+        uint8_t* vdst = kdst + KV_BYTES;
+        const uint64_t lp0 = (k_lo + uint64_t(t) * BN) / S;
+        for (int i = 0; i < ppt; ++i) {
+          const uint64_t lp = lp0 + i;
+          int row_k = -int(S) * 4;  // out of bounds -> zero fill
+          if (lp < user_pages) {
+            const uint32_t page = a.pages[R.pages_off + uint32_t(lp)];
+            row_k = int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
+          } else if (lp - user_pages < R.n_scratch && (lp - user_pages) * S < R.n_cand) {
+            const uint32_t page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
+            row_k = int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
+          }
+          const int row_v = row_k >= 0 ? row_k + int(S) : row_k;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            tma_load_2d(kdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_k, &full[st]);
+            tma_load_2d(vdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_v, &full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+      constexpr uint32_t idesc_o =
+          (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+      const uint32_t q_addr = s32(sQ), p_addr = s32(sP);
+      mbar_wait(q_full, 0);
+      tc_after();
+      auto issue_s = [&](int t) {
+        const int st = t % STAGES, sb = t & 1;
+        mbar_wait(&full[st], (t / STAGES) & 1);
+        if (t >= 2) mbar_wait(&s_free[sb], ((t / 2) - 1) & 1);
+        tc_after();
+        const uint32_t k_addr = s32(sKV + st * STAGE_BYTES);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * Smem::kBlock + (k % 4) * 32;
+          mma_f16(tmem + S_COL0 + sb * BN, sdesc(q_addr + off, 16, 1024), sdesc(k_addr + off, 16, 1024), idesc_s,
+                  k > 0);
+        }
+        mma_commit(&s_full[sb]);
+      };
+      issue_s(0);
+      for (int t = 0; t < n_tiles; ++t) {
+        if (t + 1 < n_tiles) issue_s(t + 1);
+        const int st = t % STAGES;
+        mbar_wait(p_full, t & 1);
+        tc_after();
+        const uint32_t v_addr = s32(sKV + st * STAGE_BYTES + KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) {
+          // A = P (K-major, keys contiguous): block k/4, +32 B per step
+          const uint64_t pa = sdesc(p_addr + (k / 4) * Smem::kBlock + (k % 4) * 32, 16, 1024);
+          // B = V (MN-major): 16 keys = 2 row groups of 8 -> +2048 B; dim blocks LBO = 16 KB
+          const uint64_t vb = sdesc(v_addr + k * 2048, Smem::kBlock, 1024);
+          mma_f16(tmem + O_COL, pa, vb, idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(o_done);
+        mma_commit(&empty[st]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- softmax warpgroup ----------------
+    const uint32_t r = threadIdx.x - 128;  // query row within the tile == TMEM lane
+    const uint32_t lane_base = (32u * (warp - 4)) << 16;
+    // Q row -> smem (SW128 K-major); rows past the request read finite data or zeros
+    {
+      const uint32_t qi = q0 + r;
+      const bool ok = qi < R.n_q;
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + size_t(R.q_row0 + (ok ? qi : 0)) * g.d + h * D);
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) {
+        uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(sQ + (c / 8) * Smem::kBlock + sw128(r, c % 8)) = v;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+    }
+    const uint64_t pos_r = R.start + q0 + r;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int sb = t & 1;
+      mbar_wait(&s_full[sb], (t / 2) & 1);
+      tc_after();
+      float s[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tmem + lane_base + S_COL0 + sb * BN + c * 32, s + c * 32);
+      tmem_wait_ld();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[sb]);
+      // mask + scale (log2 domain)
+      const uint64_t kb = k_lo + uint64_t(t) * BN;
+      float mx = -INFINITY;
+      const bool full_tile = (kb + BN <= KA) && (kb + BN - 1 <= pos_r) && (kb + BN <= k_hi);
+      if (full_tile) {
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          s[c] *= a.scale_log2;
+          mx = fmaxf(mx, s[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const uint64_t j = kb + c;
+          bool ok = j < k_hi;
+          uint64_t pos;
+          if (j < KAp) {
+            pos = j;
+            ok = ok && j < KA;
+          } else {
+            pos = KA + (j - KAp);
+            ok = ok && (j - KAp) < R.n_cand;
+          }
+          ok = ok && pos <= pos_r;
+          s[c] = ok ? s[c] * a.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, s[c]);
+        }
+      }
+      const float m_new = fmaxf(m_run, mx);
+      const float mref = m_new == -INFINITY ? 0.f : m_new;
+      const float alpha = m_run == -INFINITY ? 0.f : exp2f(m_run - mref);
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN; ++c) {
+        s[c] = exp2f(s[c] - mref);
+        rs += s[c];
+      }
+      l_run = l_run * alpha + rs;
+      m_run = m_new;
+      // PV of the previous tile must be done before O is rescaled / P is overwritten
+      if (t > 0) {
+        mbar_wait(o_done, (t - 1) & 1);
+        tc_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            float o[32];
+            tmem_ld32(tmem + lane_base + O_COL + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st32(tmem + lane_base + O_COL + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      // P row -> smem, bf16, SW128 K-major (2 blocks of 64 keys)
+#pragma unroll
+      for (int c = 0; c < BN / 8; ++c) {
+        uint4 v;
+        v.x = pack2(s[c * 8 + 0], s[c * 8 + 1]);
+        v.y = pack2(s[c * 8 + 2], s[c * 8 + 3]);
+        v.z = pack2(s[c * 8 + 4], s[c * 8 + 5]);
+        v.w = pack2(s[c * 8 + 6], s[c * 8 + 7]);
+        *reinterpret_cast<uint4*>(sP + (c / 8) * Smem::kBlock + sw128(r, c % 8)) = v;
+      }
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // epilogue: O / l and lse (base 2) for the split
+    const uint32_t qi = q0 + r;
+    if (n_tiles > 0) {
+      mbar_wait(o_done, (n_tiles - 1) & 1);
+      tc_after();
+    }
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    float* dst = a.part_o + (size_t(R.part_base) + size_t(it.split) * R.n_q + qi) * g.d + h * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      float o[32];
+      if (n_tiles > 0) {
+        tmem_ld32(tmem + lane_base + O_COL + c * 32, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0.f;
+      }
+      if (qi < q_end) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
+      }
+    }
+    if (qi < q_end)
+      a.part_lse[(size_t(R.part_base) + size_t(it.split) * R.n_q + qi) * g.H + h] =
+          l_run > 0.f ? m_run + log2f(l_run) : -INFINITY;
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+// ------------------------------------------------------------------ host ---
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q);
+  }
+  return fn;
+}
+
+bool attn_tc_supported(const PoolGeom& g) {
+  return (g.D == 64 || g.D == 128) && g.S >= 8 && g.S <= 128 && (128 % g.S) == 0;
+}
+
+int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
+  const cuuint64_t rows = cuuint64_t(g.L) * g.num_pages * 2 * g.S;
+  const cuuint64_t dims[2] = {g.d, rows};
+  const cuuint64_t strides[1] = {cuuint64_t(g.d) * 2};
+  const cuuint32_t box[2] = {64, g.S};
+  const cuuint32_t estr[2] = {1, 1};
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+template <int D>
+static void launch_tc_d(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {
+  constexpr size_t smem = 1024 + (D / 64) * 16384 + 32768 + STAGES * 2 * (D / 64) * 16384 + 256;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set = true;
+  }
+  attn_tc_kernel<D><<<a.n_items, 256, smem, s>>>(map, a);
+}
+
+void launch_attention_tc(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {
+  if (a.n_items == 0) return;
+  if (a.g.D == 64) launch_tc_d<64>(map, a, s);
+  else launch_tc_d<128>(map, a, s);
+}
+
+}  // namespace mtkv_b200

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 
@@ -160,6 +161,13 @@ int Engine::init(std::string& err) {
   if (kv_.bytes_per_element != 2) {
     err = "engine: the device pool stores bf16 (bytes_per_element must be 2)";
     return MTKV_ERROR;
+  }
+  // tcgen05 attention for every production shape; the mma.sync kernel covers
+  // head_dim < 64 (the reference's tiny test models). MTKV_ATTN=mma forces it
+  // for A/B measurements.
+  {
+    const char* f = std::getenv("MTKV_ATTN");
+    use_tc_ = attn_tc_supported(g_) && !(f && std::string(f) == "mma");
   }
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
@@ -340,11 +348,14 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   // ---- rows, attention work, metadata sizes ----
   std::vector<ReqDev> rd(n);
   uint32_t rows = 0, part_rows = 0, max_hist = 0, n_items = 0, ncand_total = 0;
-  constexpr uint32_t kSplitKeys = 512;
+  // tcgen05 path: 128-row query tiles over the page-padded logical key space,
+  // 1024-key splits; mma.sync path (head_dim < 64): 512-key splits over positions
+  const bool tc = use_tc_;
+  const uint32_t kSplitKeys = tc ? 1024 : 512;
   uint32_t max_q = 0;
   for (uint32_t r = 0; r < n; ++r)
     max_q = std::max(max_q, w.reqs[r].n_hist + w.reqs[r].plan.num_candidates);
-  const uint32_t bq = max_q > 64 ? 128 : 64;  // one tile covers typical fresh rows (Δ + candidates)
+  const uint32_t bq = (tc || max_q > 64) ? 128 : 64;  // one tile covers typical fresh rows (Δ + candidates)
   for (uint32_t r = 0; r < n; ++r) {
     const ReqWork& R = w.reqs[r];
     ReqDev& x = rd[r];
@@ -358,8 +369,9 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     x.scratch_off = recompute_ ? t_soff[r] : R.scratch_off;
     x.n_scratch = recompute_ ? t_ns[r] : R.n_scratch;
     x.user = R.plan.user;
-    const uint64_t T = x.start + x.n_q;
-    x.split_keys = x.n_q <= 256 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 64, 0xFFFFFFFFull));
+    const uint64_t KA = x.start + x.n_hist;
+    const uint64_t T = tc ? (KA + S - 1) / S * S + x.n_cand : x.start + x.n_q;
+    x.split_keys = x.n_q <= 256 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 128, 0xFFFFFF00ull));
     x.n_splits = uint32_t((T + x.split_keys - 1) / x.split_keys);
     x.part_base = part_rows;
     part_rows += x.n_splits * x.n_q;
@@ -555,7 +567,15 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
       aa.g = g_; aa.layer = l; aa.bq = bq; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
-      launch_attention(aa, comp_);
+      if (tc) {
+        if (pool_map_ptr_ != pool_.p) {
+          if (make_pool_map(&pool_map_, pool_.p, g_)) { err = "engine: cuTensorMapEncodeTiled failed"; return MTKV_ERROR; }
+          pool_map_ptr_ = pool_.p;
+        }
+        launch_attention_tc(pool_map_, aa, comp_);
+      } else {
+        launch_attention(aa, comp_);
+      }
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l + 1], comp_));
       ++attn_launches_last_;
       GateArgs gn{};

@@ -85,6 +85,9 @@ class Engine {
   __nv_bfloat16 *w_embed_ = nullptr, *w_in_ = nullptr, *w1_ = nullptr, *w2_ = nullptr, *w_out_ = nullptr;
   float* w_ln_ = nullptr;
   uint32_t staging_slots_ = 0;
+  bool use_tc_ = false;          // tcgen05 attention (head_dim 64/128)
+  alignas(64) CUtensorMap pool_map_{};
+  const void* pool_map_ptr_ = nullptr;
 
   // pinned host memory: slabs -> per-user extents -> chunks
   static constexpr size_t kSpareSlabs = 2;

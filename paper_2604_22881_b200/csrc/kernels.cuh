@@ -119,3 +119,11 @@ __host__ __device__ inline uint16_t tag_word(uint32_t user, uint64_t pos, uint32
 }
 
 }  // namespace mtkv_b200
+
+// ---- tcgen05 attention (attn_tc.cu): head_dim 64/128, page sizes 8..128 ----
+#include <cuda.h>
+namespace mtkv_b200 {
+bool attn_tc_supported(const PoolGeom& g);
+int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g);
+void launch_attention_tc(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s);
+}  // namespace mtkv_b200

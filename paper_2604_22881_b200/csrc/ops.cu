@@ -89,7 +89,9 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   r.part_base = 0;
   r.n_splits = 1;
   r.split_keys = 0xFFFFFFFFu;
-  const uint32_t bq = n_q > 64 ? 128 : 64;
+  const char* force = std::getenv("MTKV_ATTN");
+  const bool tc = attn_tc_supported(g) && !(force && std::string(force) == "mma");
+  const uint32_t bq = (tc || n_q > 64) ? 128 : 64;
   const uint32_t qtiles = (n_q + bq - 1) / bq, n_items = g.H * qtiles;
   AttnItem* hi = new AttnItem[n_items];
   uint32_t k = 0;
@@ -119,7 +121,19 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   a.layer = layer;
   a.bq = bq;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
-  if (e == cudaSuccess) launch_attention(a, s);
+  if (e == cudaSuccess) {
+    if (tc) {
+      alignas(64) CUtensorMap map;
+      if (make_pool_map(&map, pool, g)) {
+        cudaFreeAsync(buf, s);
+        set_last_error("paged_attention: cuTensorMapEncodeTiled failed");
+        return MTKV_ERROR;
+      }
+      launch_attention_tc(map, a, s);
+    } else {
+      launch_attention(a, s);
+    }
+  }
   cudaFreeAsync(buf, s);
   return finish(e);
 }
