@@ -105,12 +105,13 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(cfg: dict, steps: int, warmup: int, rank: int, world: int, seed: int = 1):
+def make_workload(cfg: dict, n_batches: int, rank: int, world: int, seed: int = 1):
     """Prefill requests (one 4K-token first visit per user) + revisit stream.
 
     Revisits follow the reference generator's heavy-tailed (lognormal) return
-    process (workload.cpp:85, fixed_delta=64), so recently active users come
-    back soon — the temporal locality the LRU policy exploits."""
+    process (workload.cpp:85, fixed_delta=Δ): recently active users come back
+    soon — the temporal locality the LRU policy exploits. The first part of the
+    stream is consumed as warm-up so the timed phases see the steady state."""
     import paper_2604_22881_b200 as mtkv
     rng = np.random.default_rng(seed + 7919 * rank)
     U, V = cfg["users"], cfg["vocab"]
@@ -118,7 +119,7 @@ def make_workload(cfg: dict, steps: int, warmup: int, rank: int, world: int, see
     prefill = [{"ts": 0, "user": uid(u), "dn": cfg["history"], "nc": cfg["cands"],
                 "tokens": rng.integers(0, V, cfg["history"], dtype=np.uint32),
                 "cands": rng.integers(0, V, cfg["cands"], dtype=np.uint32)} for u in range(U)]
-    n_rev = (3 * steps + warmup + 1) * cfg["batch"]
+    n_rev = n_batches * cfg["batch"]
     g = mtkv.GenConfig(num_users=U, total_requests=n_rev, fixed_delta=cfg["delta"], candidates=cfg["cands"],
                        vocab=0, mean_final_len=cfg["delta"] * 8, min_len=cfg["delta"],
                        max_len=cfg["delta"] * 64, gap_log_mu=9.0, gap_log_sigma=1.6, seed=seed + rank)
@@ -143,6 +144,18 @@ def kv_config(cfg):
                          offload_quota=cfg["chunk"] * 4 * chunks_per_batch)
 
 
+def _phase(r0, r1, steps, B):
+    req = r1["hist_required"] - r0["hist_required"]
+    dev = r1["hist_device"] - r0["hist_device"]
+    host = r1["hist_host"] - r0["hist_host"]
+    return {"gpu_hit": dev / req if req else 1.0, "total_hit": (dev + host) / req if req else 1.0,
+            "h2d_bytes_per_step": (r1["h2d_bytes"] - r0["h2d_bytes"]) / steps,
+            "d2h_bytes_per_step": (r1["d2h_bytes"] - r0["d2h_bytes"]) / steps,
+            "onload_chunks_per_step": (r1["onload_chunks"] - r0["onload_chunks"]) / steps,
+            "fresh_tokens": r1["tokens_processed"] - r0["tokens_processed"],
+            "evictions": r1["evictions"] - r0["evictions"]}
+
+
 def run_b200(args, cfg):
     import torch
     import paper_2604_22881_b200 as mtkv
@@ -156,53 +169,54 @@ def run_b200(args, cfg):
     cost = mtkv.CostModel(bus_bandwidth=55e9)  # measured pinned H2D on the B200 box (probe)
     model = mtkv.ModelConfig(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"], vocab=cfg["vocab"],
                              seed=1)
-    prefill, revisits = make_workload(cfg, args.steps, args.warmup, rank, world)
-    eng = mtkv.Engine(kv, cost, mode="hierarchical", backend="value", batch_size=cfg["batch"], model=model,
-                      device=local)
-    # ---- warm-up: prefill histories (untimed), then W revisit batches ----
+    B, K = cfg["batch"], args.steps
+    warm = args.warmup + max(args.warmup, 2 * K)  # long warm-up: timed phases see the steady state
+    prefill, revisits = make_workload(cfg, warm + 3 * K, rank, world)
+    # pinned host store sized for the run up front (no cudaHostAlloc while serving)
+    tok_bytes = kv.token_kv_bytes()
+    host_mb = int(1.3 * (cfg["users"] * (cfg["history"] + 2 * kv.chunk_size) + len(revisits) * cfg["delta"])
+                  * tok_bytes / 2**20) + 1024
+    eng = mtkv.Engine(kv, cost, mode="hierarchical", backend="value", batch_size=B, model=model,
+                      device=local, host_reserve_mb=host_mb)
+    # ---- warm-up: prefill histories (untimed), then the first revisit batches ----
     pb = max(1, 65536 // cfg["history"])
     for i in range(0, len(prefill), pb):
         eng.process_batch(prefill[i:i + pb])
-    eng.synchronize()
-    B = cfg["batch"]
-    batches = [revisits[i * B:(i + 1) * B] for i in range(args.warmup + 3 * args.steps)]
+    batches = [revisits[i * B:(i + 1) * B] for i in range(warm + 3 * K)]
     packed = [mtkv.RequestBatch(b) for b in batches]
-    for i in range(args.warmup):
+    for i in range(warm):
         eng.process_batch(None, packed=packed[i])
     eng.synchronize()
     if dist:
         dist.barrier()
 
-    # ---- timed (device throughput): requests pre-packed in host memory ----
+    # ---- phase A (value): device throughput, requests pre-packed in host memory ----
     r0 = eng.report()
+    l0 = eng.kernel_launches()
     clocks = Clocks(local)
     clocks.start()
     torch.cuda.synchronize()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record()
-    lat = []
-    wall0 = time.perf_counter()
-    for i in range(args.warmup, args.warmup + args.steps):
+    for i in range(warm, warm + K):
         eng.process_batch(None, packed=packed[i])
-        lat.append(i)
     eng.synchronize()
     t_end.record()
     torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
     clk = clocks.stop()
     r1 = eng.report()
     elapsed = t_start.elapsed_time(t_end) / 1e3
-    n_req = args.steps * B
-    fresh_tokens = r1["tokens_processed"] - r0["tokens_processed"]
+    launches_per_step = (eng.kernel_launches() - l0) / K
+    phase_a = _phase(r0, r1, K, B)
 
-    # ---- same engine, next K batches: per-batch device latency (p50/p99) and
-    #      per-launch attention timing for the roofline ----
+    # ---- phase B: per-batch device latency (p50/p99) + per-launch attention timing ----
     eng.set_profile(True)
     eng_lat, attn_ms, attn_launches, attn_bytes = [], 0.0, 0, 0
     d = cfg["H"] * cfg["D"]
-    k0 = args.warmup + args.steps
-    for i in range(k0, k0 + args.steps):
+    rb0 = eng.report()
+    k0 = warm + K
+    for i in range(k0, k0 + K):
         eng.process_batch(None, packed=packed[i])
         eng.synchronize()
         eng_lat.append(eng.last_batch_ms())
@@ -215,29 +229,24 @@ def run_b200(args, cfg):
             # per layer: K+V of every visible key once + Q (bf16) read + O (fp32) write
             attn_bytes += cfg["L"] * (keys * d * 2 * 2 + rows * d * 2 + rows * d * 4)
     eng.set_profile(False)
-    launches_per_step = None
+    phase_b = _phase(rb0, eng.report(), K, B)
 
-    # ---- same engine, next K batches end to end through the public API:
-    #      Python request dicts in (packing + H2D inside), rankings read back ----
+    # ---- phase C (e2e): public API with Python request dicts, rankings read back ----
     e0 = eng.report()
-    l0 = eng.kernel_launches()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
-    k1 = k0 + args.steps
-    for i in range(k1, k1 + args.steps):
-        eng.process_batch(batches[i])        # host dicts -> C-ABI
+    k1 = k0 + K
+    for i in range(k1, k1 + K):
+        eng.process_batch(batches[i])        # host dicts -> C-ABI (packing + H2D inside)
         _ = eng.last_rankings()              # D2H of the step's result (waits for the batch)
     eng.synchronize()
     e2e_s = time.perf_counter() - w0
-    e1 = eng.report()
-    launches_per_step = (eng.kernel_launches() - l0) / args.steps
+    phase_c = _phase(e0, eng.report(), K, B)
 
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    res = dict(elapsed=elapsed, n_req=n_req, fresh_tokens=fresh_tokens, wall=wall, e2e_s=e2e_s,
-               e2e_req=n_req, h2d=(e1["h2d_bytes"] - e0["h2d_bytes"]) / args.steps,
-               d2h=(e1["d2h_bytes"] - e0["d2h_bytes"]) / args.steps)
+    n_req, fresh_tokens = K * B, phase_a["fresh_tokens"]
     if dist:
         t = torch.tensor([elapsed, e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -251,8 +260,6 @@ def run_b200(args, cfg):
         if dist:
             dist.destroy_process_group()
         return
-    rep = r1
-    hit = dict(gpu=(rep["gpu_hit_ratio"]), total=(rep["total_hit_ratio"]))
     avg_launch_s = (attn_ms / 1e3) / max(attn_launches, 1)
     achieved = (attn_bytes / max(attn_launches, 1)) / avg_launch_s / 1e9 if attn_launches else 0.0
     line = {
@@ -260,9 +267,9 @@ def run_b200(args, cfg):
         "value": n_all / elapsed,
         "unit": "requests/s",
         "n_gpus": world,
-        "steps": args.steps,
+        "steps": K,
         "warmup": args.warmup,
-        "ms_per_step": elapsed / args.steps * 1e3,
+        "ms_per_step": elapsed / K * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -274,20 +281,23 @@ def run_b200(args, cfg):
                                f"pinned-host tier, hierarchical",
                    "users_per_gpu": cfg["users"], "batch": B, "device_pages": kv.device_pages,
                    "page_size": cfg["page"], "chunk_size": cfg["chunk"], "parallelism": f"user-shard x{world}",
+                   "warmup_batches_effective": warm,
                    "l2": "inputs larger than L2 (KV working set >> 126 MB)"},
         "tokens_per_sec": tok_all / elapsed,
         "p50_batch_ms": float(np.percentile(eng_lat, 50)) if eng_lat else None,
         "p99_batch_ms": float(np.percentile(eng_lat, 99)) if eng_lat else None,
-        "hit_ratio": {"gpu": rep["gpu_hit_ratio"], "total": rep["total_hit_ratio"],
-                      "note": "cumulative over prefill + warm-up + timed steps"},
-        "e2e": {"value": n_all / e2e_s, "unit": "requests/s", "h2d_bytes_per_step": res["h2d"],
-                "d2h_bytes_per_step": res["d2h"]},
-        "gpu_launches": int(round(launches_per_step * args.steps)),
+        "hit_ratio": {"gpu": phase_a["gpu_hit"], "total": phase_a["total_hit"], "note": "timed phase A"},
+        "phases": {"A_device": phase_a, "B_latency": phase_b, "C_e2e": phase_c},
+        "e2e": {"value": n_all / e2e_s, "unit": "requests/s", "h2d_bytes_per_step": phase_c["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": phase_c["d2h_bytes_per_step"]},
+        "gpu_launches": int(round(launches_per_step * K)),
         "gpu_launches_per_step": launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
-                     "kernel": "attn_kernel (paged incremental attention)",
-                     "launches_timed": attn_launches},
+                     "kernel": "attn_tc_kernel (tcgen05 paged incremental attention)",
+                     "launches_timed": attn_launches,
+                     "avg_launch_us": avg_launch_s * 1e6,
+                     "bytes_per_launch": attn_bytes / max(attn_launches, 1)},
         "clocks": clk,
     }
     if args.cpu_baseline:

@@ -97,6 +97,8 @@ typedef struct {
   double clock;
   /* measured on the device (0 for a planner without executor) */
   uint64_t h2d_bytes, d2h_bytes, onload_chunks, offload_chunks;
+  /* raw hit accounting behind the ratios (sim.hpp:70 HitAccumulator) */
+  uint64_t hist_required, hist_device, hist_host;
 } mtkv_run_report;
 
 typedef struct {
@@ -110,6 +112,7 @@ typedef struct {
   uint32_t max_user_pages;   /* 0 = device_pages */
   uint32_t keep_logits;      /* 1: keep full [n x vocab] logits of the last batch */
   uint32_t profile;          /* 1: time every attention launch with CUDA events */
+  uint64_t host_reserve_mb;  /* pinned host store allocated up front (0: grow on demand) */
 } mtkv_engine_options;
 
 /* ---- configuration (core.cpp) ---- */

@@ -98,14 +98,15 @@ class _Report(C.Structure):
                 ("occupied_pages", C.c_uint64), ("free_pages", C.c_uint64),
                 ("quota_in_flight", C.c_uint64), ("clock", C.c_double), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("onload_chunks", C.c_uint64),
-                ("offload_chunks", C.c_uint64)]
+                ("offload_chunks", C.c_uint64), ("hist_required", C.c_uint64),
+                ("hist_device", C.c_uint64), ("hist_host", C.c_uint64)]
 
 
 class _EngineOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("backend", C.c_int), ("batch_size", C.c_uint32),
                 ("seed", C.c_uint64), ("model", _ModelCfg), ("device", C.c_int),
                 ("max_batch_tokens", C.c_uint32), ("max_user_pages", C.c_uint32),
-                ("keep_logits", C.c_uint32), ("profile", C.c_uint32)]
+                ("keep_logits", C.c_uint32), ("profile", C.c_uint32), ("host_reserve_mb", C.c_uint64)]
 
 
 class _GenCfg(C.Structure):
@@ -458,7 +459,8 @@ class Engine(_ManagerView):
 
     def __init__(self, kv: KVConfig, cost: CostModel | None = None, mode: str = "hierarchical",
                  backend: str = "tag", batch_size: int = 1, model: ModelConfig | None = None,
-                 device: int = 0, keep_logits: bool = False, profile: bool = False, seed: int = 1):
+                 device: int = 0, keep_logits: bool = False, profile: bool = False, seed: int = 1,
+                 host_reserve_mb: int = 0):
         self.kv, self.mode, self.backend, self.batch_size = kv, mode, backend, batch_size
         self.model = model
         if backend == "value" and model is None:
@@ -468,6 +470,7 @@ class Engine(_ManagerView):
         if model is not None:
             o.model = _ModelCfg(model.num_layers, model.num_heads, model.head_dim, model.vocab, model.seed)
         o.device, o.keep_logits, o.profile = device, int(keep_logits), int(profile)
+        o.host_reserve_mb = int(host_reserve_mb)
         self._h = lib().mtkv_engine_create(C.byref(kv._c()), C.byref((cost or CostModel())._c()),
                                            C.byref(o))
         if not self._h:

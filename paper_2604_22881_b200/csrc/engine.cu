@@ -199,8 +199,19 @@ int Engine::init(std::string& err) {
   }
   // host extents of ~8 MB (>= 1 chunk) and slabs of >= 4 extents
   chunks_per_extent_ = uint32_t(std::max<size_t>(1, (size_t(8) << 20) / chunk_bytes_));
-  slab_bytes_ = std::max<size_t>(size_t(256) << 20, chunk_bytes_ * chunks_per_extent_ * 4);
-  if (opt_.mode == MTKV_MODE_HIERARCHICAL) refill_ = std::thread([this] { slab_refill_loop(); });
+  slab_bytes_ = std::max<size_t>(size_t(64) << 20, chunk_bytes_ * chunks_per_extent_ * 4);
+  if (opt_.mode == MTKV_MODE_HIERARCHICAL) {
+    // reserve the expected host store now: cudaHostAlloc takes the driver lock
+    // and would stall launches if it ran while serving
+    const size_t want = size_t(opt_.host_reserve_mb) << 20;
+    for (size_t got = 0; got < want; got += slab_bytes_) {
+      char* s = nullptr;
+      CK(cudaHostAlloc((void**)&s, slab_bytes_, cudaHostAllocDefault));
+      slabs_.push_back(s);
+      spare_slabs_.push_back(s);
+    }
+    refill_ = std::thread([this] { slab_refill_loop(); });
+  }
   // staging for the largest onload a batch may plan (KVConfig::onload_pages),
   // allocated up front so no timed batch reallocates (capped; grows lazily past it)
   if (opt_.mode == MTKV_MODE_HIERARCHICAL) {

@@ -453,12 +453,41 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
 
 // ------------------------------------------------------------- gate/norm ---
 // One warp per fresh row: merge split-K partials, silu(o) * u, layer norm.
-__global__ void gate_norm_kernel(GateArgs a) {
-  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+constexpr int GATE_WARPS = 8, GATE_MAXW = 256;  // per-warp cache of split weights
+
+__global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) {
+  __shared__ float wsm[GATE_WARPS][GATE_MAXW];
+  const int wid = threadIdx.x / 32;
+  const int row = blockIdx.x * GATE_WARPS + wid;
   const int lane = threadIdx.x & 31;
   if (row >= (int)a.rows) return;
   const ReqDev R = a.reqs[a.row_req[row]];
   const uint32_t i = row - R.q_row0, d = a.H * a.D;
+  const uint32_t nw = R.n_splits * a.H;
+  const bool cached = nw <= GATE_MAXW;
+  float* w = wsm[wid];
+  if (cached) {
+    // normalised merge weights w[s*H+h] = 2^(lse_s,h - max_s) / sum_s(...)
+    for (uint32_t p = lane; p < nw; p += 32) {
+      const uint32_t sp = p / a.H, h = p % a.H;
+      w[p] = a.part_lse[((size_t)R.part_base + (size_t)sp * R.n_q + i) * a.H + h];
+    }
+    __syncwarp();
+    for (uint32_t h = lane; h < a.H; h += 32) {
+      float mx = -INFINITY;
+      for (uint32_t sp = 0; sp < R.n_splits; ++sp) mx = fmaxf(mx, w[sp * a.H + h]);
+      float den = 0.f;
+      for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
+        const float l = w[sp * a.H + h];
+        const float e = l == -INFINITY ? 0.f : exp2f(l - mx);
+        w[sp * a.H + h] = e;
+        den += e;
+      }
+      const float inv = den > 0.f ? 1.f / den : 0.f;
+      for (uint32_t sp = 0; sp < R.n_splits; ++sp) w[sp * a.H + h] *= inv;
+    }
+    __syncwarp();
+  }
   constexpr int MAXE = 16;  // d <= 512
   float x[MAXE];
   float sum = 0.f;
@@ -468,19 +497,27 @@ __global__ void gate_norm_kernel(GateArgs a) {
     x[e] = 0.f;
     if (j >= d) continue;
     const uint32_t h = j / a.D;
-    float mx = -INFINITY;
-    for (uint32_t sp = 0; sp < R.n_splits; ++sp)
-      mx = fmaxf(mx, a.part_lse[((size_t)R.part_base + sp * R.n_q + i) * a.H + h]);
-    float num = 0.f, den = 0.f;
-    for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
-      const size_t prow = (size_t)R.part_base + sp * R.n_q + i;
-      const float l = a.part_lse[prow * a.H + h];
-      if (l == -INFINITY) continue;
-      const float w = exp2f(l - mx);
-      num += w * a.part_o[prow * d + j];
-      den += w;
+    float o = 0.f;
+    if (cached) {
+      for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
+        const float ws = w[sp * a.H + h];
+        if (ws != 0.f) o += ws * a.part_o[((size_t)R.part_base + (size_t)sp * R.n_q + i) * d + j];
+      }
+    } else {
+      float mx = -INFINITY;
+      for (uint32_t sp = 0; sp < R.n_splits; ++sp)
+        mx = fmaxf(mx, a.part_lse[((size_t)R.part_base + sp * R.n_q + i) * a.H + h]);
+      float num = 0.f, den = 0.f;
+      for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
+        const size_t prow = (size_t)R.part_base + sp * R.n_q + i;
+        const float l = a.part_lse[prow * a.H + h];
+        if (l == -INFINITY) continue;
+        const float ws = exp2f(l - mx);
+        num += ws * a.part_o[prow * d + j];
+        den += ws;
+      }
+      o = den > 0.f ? num / den : 0.f;
     }
-    const float o = den > 0.f ? num / den : 0.f;
     const float u = __bfloat162float(a.u[(size_t)row * d + j]);
     x[e] = (o / (1.0f + expf(-o))) * u;
     sum += x[e];
@@ -507,7 +544,7 @@ __global__ void gate_norm_kernel(GateArgs a) {
 
 void launch_gate_norm(const GateArgs& a, cudaStream_t s) {
   if (a.rows == 0) return;
-  gate_norm_kernel<<<(a.rows + 3) / 4, 128, 0, s>>>(a);
+  gate_norm_kernel<<<(a.rows + GATE_WARPS - 1) / GATE_WARPS, GATE_WARPS * 32, 0, s>>>(a);
 }
 
 // -------------------------------------------------------- scatter/gather ---

@@ -462,6 +462,9 @@ void Planner::report(mtkv_run_report& r) const {
   r.free_pages = free_.size();
   r.quota_in_flight = quota_used_;
   r.clock = clock_;
+  r.hist_required = required_;
+  r.hist_device = dev_served_;
+  r.hist_host = host_served_;
 }
 
 }  // namespace mtkv_b200
