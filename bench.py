@@ -120,15 +120,37 @@ def make_workload(cfg: dict, n_batches: int, rank: int, world: int, seed: int = 
                 "tokens": rng.integers(0, V, cfg["history"], dtype=np.uint32),
                 "cands": rng.integers(0, V, cfg["cands"], dtype=np.uint32)} for u in range(U)]
     n_rev = n_batches * cfg["batch"]
-    g = mtkv.GenConfig(num_users=U, total_requests=n_rev, fixed_delta=cfg["delta"], candidates=cfg["cands"],
-                       vocab=0, mean_final_len=cfg["delta"] * 8, min_len=cfg["delta"],
-                       max_len=cfg["delta"] * 64, gap_log_mu=9.0, gap_log_sigma=1.6, seed=seed + rank)
     revisits = []
-    for r in mtkv.generate_trace(g)[:n_rev]:
-        revisits.append({"ts": r["ts"], "user": uid(r["user"]), "dn": cfg["delta"], "nc": cfg["cands"],
+    for ts, u in stationary_revisits(U, n_rev, rng):
+        revisits.append({"ts": int(ts), "user": uid(int(u)), "dn": cfg["delta"], "nc": cfg["cands"],
                          "tokens": rng.integers(0, V, cfg["delta"], dtype=np.uint32),
                          "cands": rng.integers(0, V, cfg["cands"], dtype=np.uint32)})
     return prefill, revisits
+
+
+def stationary_revisits(U: int, n: int, rng, mu: float = 9.0, sigma: float = 1.6):
+    """Per-user renewal processes with lognormal return gaps (ms) — the heavy
+    tail of the paper's Fig. 5 and of the reference presets (workload.cpp:28,
+    gap_log_mu=9, gap_log_sigma=1.6) — merged in time, observed after a burn-in
+    of several mean gaps so the window is stationary (the reference generator's
+    fixed horizon is not: its traffic ramps up and down)."""
+    mean_gap = np.exp(mu + sigma ** 2 / 2)
+    window = n * mean_gap / U * 1.05
+    t0 = 6 * mean_gap
+    horizon = t0 + window
+    per_user = int(horizon / mean_gap * 1.6) + 32
+    gaps = np.exp(rng.normal(mu, sigma, size=(U, per_user)))
+    times = np.cumsum(gaps, axis=1) - rng.uniform(0, mean_gap, size=(U, 1))
+    users = np.broadcast_to(np.arange(U)[:, None], times.shape)
+    sel = (times >= t0) & (times < horizon)
+    t, u = times[sel], users[sel]
+    order = np.argsort(t, kind="stable")
+    t, u = t[order][:n], u[order][:n]
+    if len(t) < n:  # extremely unlikely; pad by recycling the window
+        reps = -(-n // len(t))
+        t = np.concatenate([t + k * window for k in range(reps)])[:n]
+        u = np.tile(u, reps)[:n]
+    return zip(t - t0, u)
 
 
 def kv_config(cfg):
@@ -199,9 +221,11 @@ def run_b200(args, cfg):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects these launches
     for i in range(warm, warm + K):
         eng.process_batch(None, packed=packed[i])
     eng.synchronize()
+    torch.cuda.nvtx.range_pop()
     t_end.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
