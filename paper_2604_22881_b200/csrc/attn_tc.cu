@@ -50,6 +50,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(s32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -186,31 +195,44 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0 && n_tiles > 0) {
-      const int ppt = BN / S;  // pages per tile
+    // ---------------- TMA producer (whole warp: lane i resolves page i) ----------------
+    if (n_tiles > 0) {
+      const int ppt = BN / S;  // pages per tile (<= 16)
+      // pool row of the K slice of logical page lp (out of bounds -> TMA zero fill)
+      auto row_of = [&](uint64_t lp) -> int {
+        if (lp < user_pages) {
+          const uint32_t page = a.pages[R.pages_off + uint32_t(lp)];
+          return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
+        }
+        if (lp - user_pages < R.n_scratch && (lp - user_pages) * S < R.n_cand) {
+          const uint32_t page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
+          return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
+        }
+        return -int(S) * 4;
+      };
+      const uint64_t lp_base = k_lo / S;
+      int row_next = lane < uint32_t(ppt) ? row_of(lp_base + lane) : 0;
       for (int t = 0; t < n_tiles; ++t) {
         const int st = t % STAGES;
-        if (t >= STAGES) mbar_wait(&empty[st], ((t / STAGES) - 1) & 1);
-        mbar_expect_tx(&full[st], STAGE_BYTES);
+        const int row_cur = row_next;
+        // page ids of the next tile are fetched while this tile's stage frees up
+        if (t + 1 < n_tiles && lane < uint32_t(ppt)) row_next = row_of(lp_base + uint64_t(t + 1) * ppt + lane);
+        if (lane == 0) {
+          if (t >= STAGES) mbar_wait(&empty[st], ((t / STAGES) - 1) & 1);
+          mbar_expect_tx(&full[st], STAGE_BYTES);
+        }
+        __syncwarp();
         uint8_t* kdst = sKV + st * STAGE_BYTES;
         uint8_t* vdst = kdst + KV_BYTES;
-        const uint64_t lp0 = (k_lo + uint64_t(t) * BN) / S;
         for (int i = 0; i < ppt; ++i) {
-          const uint64_t lp = lp0 + i;
-          int row_k = -int(S) * 4;  // out of bounds -> zero fill
-          if (lp < user_pages) {
-            const uint32_t page = a.pages[R.pages_off + uint32_t(lp)];
-            row_k = int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
-          } else if (lp - user_pages < R.n_scratch && (lp - user_pages) * S < R.n_cand) {
-            const uint32_t page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
-            row_k = int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
-          }
+          const int row_k = __shfl_sync(0xffffffffu, row_cur, i);
           const int row_v = row_k >= 0 ? row_k + int(S) : row_k;
+          if (lane == 0) {
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            tma_load_2d(kdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_k, &full[st]);
-            tma_load_2d(vdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_v, &full[st]);
+            for (int b = 0; b < NB; ++b) {
+              tma_load_2d(kdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_k, &full[st]);
+              tma_load_2d(vdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_v, &full[st]);
+            }
           }
         }
       }
@@ -239,8 +261,13 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         mma_commit(&s_full[sb]);
       };
       issue_s(0);
+      int s_issued = 1;  // S tiles issued so far
       for (int t = 0; t < n_tiles; ++t) {
-        if (t + 1 < n_tiles) issue_s(t + 1);
+        // S(t+1) overlaps softmax(t) when its K tile has landed; PV(t) must not wait for it
+        if (s_issued == t + 1 && t + 1 < n_tiles && mbar_ready(&full[(t + 1) % STAGES], ((t + 1) / STAGES) & 1)) {
+          issue_s(t + 1);
+          ++s_issued;
+        }
         const int st = t % STAGES;
         mbar_wait(p_full, t & 1);
         tc_after();
@@ -255,6 +282,10 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         }
         mma_commit(o_done);
         mma_commit(&empty[st]);
+        if (s_issued == t + 1 && t + 1 < n_tiles) {
+          issue_s(t + 1);
+          ++s_issued;
+        }
       }
     }
   } else if (warp >= 4) {

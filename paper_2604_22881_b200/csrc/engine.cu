@@ -500,8 +500,11 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       }
       int64_t b = chunk_d2h_batch_[m.chunk_id];
       while (j + run < n_on) {
+        // same user, next chunk, same extent (one pinned allocation per copy)
         const ChunkMove& nx = w.onloads[j + run];
-        if (nx.chunk_id >= chunk_ptr_.size() || chunk_ptr_[nx.chunk_id] != chunk_ptr_[m.chunk_id] + run * chunk_bytes_)
+        if (nx.user != m.user || nx.chunk_index != m.chunk_index + run ||
+            nx.chunk_index / chunks_per_extent_ != m.chunk_index / chunks_per_extent_ ||
+            nx.chunk_id >= chunk_ptr_.size() || chunk_ptr_[nx.chunk_id] != chunk_ptr_[m.chunk_id] + run * chunk_bytes_)
           break;
         b = std::max(b, chunk_d2h_batch_[nx.chunk_id]);
         ++run;

@@ -564,9 +564,24 @@ __global__ void chunk_copy_kernel(__nv_bfloat16* pool, __nv_bfloat16* staging, c
   __nv_bfloat16* pp = pool + g.off(l, page, kv, 0);
   __nv_bfloat16* sp = staging + ((((size_t)w.slot * g.L + l) * 2 + kv) * g.chunk + (size_t)p * g.S) * g.d;
   if ((seg % 8) == 0) {
+    // all loads of a thread in flight before its stores (8 x 16 B per thread)
+    constexpr int U = 8;
     uint4* dst = reinterpret_cast<uint4*>(TO_POOL ? pp : sp);
     const uint4* src = reinterpret_cast<const uint4*>(TO_POOL ? sp : pp);
-    for (size_t i = threadIdx.x; i < seg / 8; i += blockDim.x) dst[i] = src[i];
+    const size_t n = seg / 8;
+    for (size_t base = threadIdx.x; base < n; base += (size_t)blockDim.x * U) {
+      uint4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t idx = base + (size_t)u * blockDim.x;
+        if (idx < n) r[u] = __ldcs(src + idx);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t idx = base + (size_t)u * blockDim.x;
+        if (idx < n) dst[idx] = r[u];
+      }
+    }
   } else {
     __nv_bfloat16* dst = TO_POOL ? pp : sp;
     const __nv_bfloat16* src = TO_POOL ? sp : pp;
@@ -578,14 +593,14 @@ void launch_scatter_chunks(__nv_bfloat16* pool, const __nv_bfloat16* staging, co
                            const uint32_t* pages, uint32_t n_chunks, const PoolGeom& g, cudaStream_t s) {
   if (!n_chunks) return;
   const uint32_t blocks = n_chunks * g.L * 2 * (g.chunk / g.S);
-  chunk_copy_kernel<true><<<blocks, 256, 0, s>>>(pool, const_cast<__nv_bfloat16*>(staging), work, pages, g);
+  chunk_copy_kernel<true><<<blocks, 128, 0, s>>>(pool, const_cast<__nv_bfloat16*>(staging), work, pages, g);
 }
 
 void launch_gather_chunks(__nv_bfloat16* staging, const __nv_bfloat16* pool, const ChunkWork* work,
                           const uint32_t* pages, uint32_t n_chunks, const PoolGeom& g, cudaStream_t s) {
   if (!n_chunks) return;
   const uint32_t blocks = n_chunks * g.L * 2 * (g.chunk / g.S);
-  chunk_copy_kernel<false><<<blocks, 256, 0, s>>>(const_cast<__nv_bfloat16*>(pool), staging, work, pages, g);
+  chunk_copy_kernel<false><<<blocks, 128, 0, s>>>(const_cast<__nv_bfloat16*>(pool), staging, work, pages, g);
 }
 
 // -------------------------------------------------------------- tag mode ---
