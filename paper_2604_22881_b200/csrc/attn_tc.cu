@@ -28,8 +28,8 @@ namespace mtkv_b200 {
 namespace tc {
 
 constexpr int BM = 128;   // query rows per tile (TMEM lanes)
-constexpr int BN = 128;   // keys per tile
-constexpr int STAGES = 2;
+constexpr int BN = 64;    // keys per tile
+constexpr int STAGES = 4; // K+V ring depth
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -114,6 +114,12 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // byte offset of 16-byte chunk `c` (of 8) in row `r` of a SW128 K-major block
 __device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -129,13 +135,16 @@ using namespace tc;
 
 template <int D>
 __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, AttnArgs a) {
-  constexpr int NB = D / 64;                      // 64-element column blocks of Q/K/V
-  constexpr uint32_t Q_BYTES = NB * Smem::kBlock;  // 128 rows x D
-  constexpr uint32_t P_BYTES = 2 * Smem::kBlock;   // 128 rows x 128 keys
-  constexpr uint32_t KV_BYTES = NB * Smem::kBlock; // 128 keys x D (K or V)
+  constexpr int NB = D / 64;                            // 64-element column blocks of Q/K/V
+  constexpr uint32_t QBLK = BM * 128;                   // Q/P block: 128 rows x 128 B
+  constexpr uint32_t KBLK = BN * 128;                   // K/V block: BN rows x 128 B
+  constexpr uint32_t Q_BYTES = NB * QBLK;
+  constexpr uint32_t P_BYTES = (BN / 64) * QBLK;        // 128 rows x BN keys
+  constexpr uint32_t KV_BYTES = NB * KBLK;              // BN keys x D (K or V)
   constexpr uint32_t STAGE_BYTES = 2 * KV_BYTES;
-  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t TMEM_COLS = (2 * BN + D) <= 256 ? 256 : 512;
   constexpr uint32_t S_COL0 = 0, O_COL = 2 * BN;
+  constexpr float kRescale = 8.f;                       // lazy rescale threshold (log2 units)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -143,13 +152,13 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
   uint8_t* sP = sQ + Q_BYTES;
   uint8_t* sKV = sP + P_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;              // [STAGES]
-  uint64_t* empty = bars + STAGES;    // [STAGES]
-  uint64_t* s_full = bars + 2 * STAGES;      // [2]
-  uint64_t* s_free = s_full + 2;             // [2]
-  uint64_t* p_full = s_free + 2;
-  uint64_t* o_done = p_full + 1;
-  uint64_t* q_full = o_done + 1;
+  uint64_t* full = bars;                 // [STAGES] K+V of a tile landed
+  uint64_t* empty = bars + STAGES;       // [STAGES] stage consumed by PV
+  uint64_t* s_full = bars + 2 * STAGES;  // [2] S tile in TMEM
+  uint64_t* s_free = s_full + 2;         // [2] S tile read by softmax
+  uint64_t* p_full = s_free + 2;         // P in smem (+ O rescaled)
+  uint64_t* o_done = p_full + 1;         // PV committed
+  uint64_t* q_full = o_done + 1;         // Q in smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
   const AttnItem it = a.items[blockIdx.x];
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
   if (warp == 0) {
     // ---------------- TMA producer (whole warp: lane i resolves page i) ----------------
     if (n_tiles > 0) {
-      const int ppt = BN / S;  // pages per tile (<= 16)
+      const int ppt = BN / S;  // pages per tile
       // pool row of the K slice of logical page lp (out of bounds -> TMA zero fill)
       auto row_of = [&](uint64_t lp) -> int {
         if (lp < user_pages) {
@@ -211,12 +220,15 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         return -int(S) * 4;
       };
       const uint64_t lp_base = k_lo / S;
-      int row_next = lane < uint32_t(ppt) ? row_of(lp_base + lane) : 0;
+      // lanes cover 32 consecutive pages; refreshed every 32/ppt tiles
+      int rows_cache = row_of(lp_base + lane);
+      int cache_tile0 = 0;
       for (int t = 0; t < n_tiles; ++t) {
         const int st = t % STAGES;
-        const int row_cur = row_next;
-        // page ids of the next tile are fetched while this tile's stage frees up
-        if (t + 1 < n_tiles && lane < uint32_t(ppt)) row_next = row_of(lp_base + uint64_t(t + 1) * ppt + lane);
+        if ((t - cache_tile0) * ppt >= 32) {
+          cache_tile0 = t;
+          rows_cache = row_of(lp_base + uint64_t(t) * ppt + lane);
+        }
         if (lane == 0) {
           if (t >= STAGES) mbar_wait(&empty[st], ((t / STAGES) - 1) & 1);
           mbar_expect_tx(&full[st], STAGE_BYTES);
@@ -225,13 +237,13 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         uint8_t* kdst = sKV + st * STAGE_BYTES;
         uint8_t* vdst = kdst + KV_BYTES;
         for (int i = 0; i < ppt; ++i) {
-          const int row_k = __shfl_sync(0xffffffffu, row_cur, i);
+          const int row_k = __shfl_sync(0xffffffffu, rows_cache, (t - cache_tile0) * ppt + i);
           const int row_v = row_k >= 0 ? row_k + int(S) : row_k;
           if (lane == 0) {
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-              tma_load_2d(kdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_k, &full[st]);
-              tma_load_2d(vdst + b * Smem::kBlock + i * S * 128, &pool_map, int(h * D + 64 * b), row_v, &full[st]);
+              tma_load_2d(kdst + b * KBLK + i * S * 128, &pool_map, int(h * D + 64 * b), row_k, &full[st]);
+              tma_load_2d(vdst + b * KBLK + i * S * 128, &pool_map, int(h * D + 64 * b), row_v, &full[st]);
             }
           }
         }
@@ -253,11 +265,9 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         tc_after();
         const uint32_t k_addr = s32(sKV + st * STAGE_BYTES);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * Smem::kBlock + (k % 4) * 32;
-          mma_f16(tmem + S_COL0 + sb * BN, sdesc(q_addr + off, 16, 1024), sdesc(k_addr + off, 16, 1024), idesc_s,
-                  k > 0);
-        }
+        for (int k = 0; k < D / 16; ++k)
+          mma_f16(tmem + S_COL0 + sb * BN, sdesc(q_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024),
+                  sdesc(k_addr + (k / 4) * KBLK + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
         mma_commit(&s_full[sb]);
       };
       issue_s(0);
@@ -275,9 +285,9 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k) {
           // A = P (K-major, keys contiguous): block k/4, +32 B per step
-          const uint64_t pa = sdesc(p_addr + (k / 4) * Smem::kBlock + (k % 4) * 32, 16, 1024);
-          // B = V (MN-major): 16 keys = 2 row groups of 8 -> +2048 B; dim blocks LBO = 16 KB
-          const uint64_t vb = sdesc(v_addr + k * 2048, Smem::kBlock, 1024);
+          const uint64_t pa = sdesc(p_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024);
+          // B = V (MN-major): 16 keys = 2 row groups of 8 -> +2048 B; dim blocks LBO = KBLK
+          const uint64_t vb = sdesc(v_addr + k * 2048, KBLK, 1024);
           mma_f16(tmem + O_COL, pa, vb, idesc_o, (t > 0 || k > 0) ? 1u : 0u);
         }
         mma_commit(o_done);
@@ -300,14 +310,17 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
 #pragma unroll
       for (int c = 0; c < D / 8; ++c) {
         uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sQ + (c / 8) * Smem::kBlock + sw128(r, c % 8)) = v;
+        *reinterpret_cast<uint4*>(sQ + (c / 8) * QBLK + sw128(r, c % 8)) = v;
       }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(q_full);
     }
     const uint64_t pos_r = R.start + q0 + r;
-    float m_run = -INFINITY, l_run = 0.f;
+    // valid keys of this row: user keys [0, u_end), candidate keys [KAp, c_end)
+    const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
+    const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
+    float m_ref = -INFINITY, l_run = 0.f;
     for (int t = 0; t < n_tiles; ++t) {
       const int sb = t & 1;
       mbar_wait(&s_full[sb], (t / 2) & 1);
@@ -319,11 +332,13 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[sb]);
-      // mask + scale (log2 domain)
+      // mask (two half-open ranges relative to the tile) + scale, base 2
       const uint64_t kb = k_lo + uint64_t(t) * BN;
+      const int cu = int(u_end > kb ? (u_end - kb < uint64_t(BN) ? u_end - kb : uint64_t(BN)) : 0);
+      const int c_lo = int(KAp > kb ? (KAp - kb < uint64_t(BN) ? KAp - kb : uint64_t(BN)) : 0);
+      const int c_hi = int(c_end > kb ? (c_end - kb < uint64_t(BN) ? c_end - kb : uint64_t(BN)) : 0);
       float mx = -INFINITY;
-      const bool full_tile = (kb + BN <= KA) && (kb + BN - 1 <= pos_r) && (kb + BN <= k_hi);
-      if (full_tile) {
+      if (cu == BN) {
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
           s[c] *= a.scale_log2;
@@ -332,32 +347,26 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
       } else {
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
-          const uint64_t j = kb + c;
-          bool ok = j < k_hi;
-          uint64_t pos;
-          if (j < KAp) {
-            pos = j;
-            ok = ok && j < KA;
-          } else {
-            pos = KA + (j - KAp);
-            ok = ok && (j - KAp) < R.n_cand;
-          }
-          ok = ok && pos <= pos_r;
+          const bool ok = c < cu || (c >= c_lo && c < c_hi);
           s[c] = ok ? s[c] * a.scale_log2 : -INFINITY;
           mx = fmaxf(mx, s[c]);
         }
       }
-      const float m_new = fmaxf(m_run, mx);
-      const float mref = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = m_run == -INFINITY ? 0.f : exp2f(m_run - mref);
+      // lazy rescale: keep the reference max unless the new max exceeds it by
+      // more than 2^8 (p <= 256 stays exact enough in fp32/bf16)
+      float alpha = 1.f;
+      if (mx > m_ref + kRescale) {
+        alpha = m_ref == -INFINITY ? 0.f : ex2(m_ref - mx);
+        m_ref = mx;
+      }
+      const float mref = m_ref == -INFINITY ? 0.f : m_ref;
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < BN; ++c) {
-        s[c] = exp2f(s[c] - mref);
+        s[c] = ex2(s[c] - mref);
         rs += s[c];
       }
       l_run = l_run * alpha + rs;
-      m_run = m_new;
       // PV of the previous tile must be done before O is rescaled / P is overwritten
       if (t > 0) {
         mbar_wait(o_done, (t - 1) & 1);
@@ -375,7 +384,7 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
           tmem_wait_st();
         }
       }
-      // P row -> smem, bf16, SW128 K-major (2 blocks of 64 keys)
+      // P row -> smem, bf16, SW128 K-major (blocks of 64 keys)
 #pragma unroll
       for (int c = 0; c < BN / 8; ++c) {
         uint4 v;
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         v.y = pack2(s[c * 8 + 2], s[c * 8 + 3]);
         v.z = pack2(s[c * 8 + 4], s[c * 8 + 5]);
         v.w = pack2(s[c * 8 + 6], s[c * 8 + 7]);
-        *reinterpret_cast<uint4*>(sP + (c / 8) * Smem::kBlock + sw128(r, c % 8)) = v;
+        *reinterpret_cast<uint4*>(sP + (c / 8) * QBLK + sw128(r, c % 8)) = v;
       }
       fence_async_smem();
       tc_before();
@@ -416,7 +425,7 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
     }
     if (qi < q_end)
       a.part_lse[(size_t(R.part_base) + size_t(it.split) * R.n_q + qi) * g.H + h] =
-          l_run > 0.f ? m_run + log2f(l_run) : -INFINITY;
+          l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
   }
   tc_before();
   __syncthreads();
@@ -454,7 +463,7 @@ int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
 
 template <int D>
 static void launch_tc_d(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {
-  constexpr size_t smem = 1024 + (D / 64) * 16384 + 32768 + STAGES * 2 * (D / 64) * 16384 + 256;
+  constexpr size_t smem = 1024 + (D / 64) * BM * 128 + (BN / 64) * BM * 128 + STAGES * 2 * (D / 64) * BN * 128 + 256;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
