@@ -133,32 +133,37 @@ struct Smem {
 
 using namespace tc;
 
+// Two softmax pipelines per CTA: warpgroup p in {0,1} owns key tiles t with
+// t % 2 == p, its own S and O accumulators in TMEM and its own P buffer, and
+// writes its result as partial (2*split + p); the split-K merge in
+// gate_norm_kernel combines them. While one warpgroup runs softmax the tensor
+// core works on the other pipeline's S / PV, so neither unit waits on the other.
 template <int D>
-__global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, AttnArgs a) {
+__global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, AttnArgs a) {
   constexpr int NB = D / 64;                            // 64-element column blocks of Q/K/V
   constexpr uint32_t QBLK = BM * 128;                   // Q/P block: 128 rows x 128 B
   constexpr uint32_t KBLK = BN * 128;                   // K/V block: BN rows x 128 B
   constexpr uint32_t Q_BYTES = NB * QBLK;
-  constexpr uint32_t P_BYTES = (BN / 64) * QBLK;        // 128 rows x BN keys
+  constexpr uint32_t P_BYTES = (BN / 64) * QBLK;        // 128 rows x BN keys (per pipeline)
   constexpr uint32_t KV_BYTES = NB * KBLK;              // BN keys x D (K or V)
   constexpr uint32_t STAGE_BYTES = 2 * KV_BYTES;
-  constexpr uint32_t TMEM_COLS = (2 * BN + D) <= 256 ? 256 : 512;
-  constexpr uint32_t S_COL0 = 0, O_COL = 2 * BN;
+  constexpr uint32_t PIPE_COLS = BN + D;                // S + O per pipeline
+  constexpr uint32_t TMEM_COLS = 2 * PIPE_COLS <= 256 ? 256 : 512;
   constexpr float kRescale = 8.f;                       // lazy rescale threshold (log2 units)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sP = sQ + Q_BYTES;
-  uint8_t* sKV = sP + P_BYTES;
+  uint8_t* sP = sQ + Q_BYTES;                 // [2] pipelines
+  uint8_t* sKV = sP + 2 * P_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + STAGES * STAGE_BYTES);
   uint64_t* full = bars;                 // [STAGES] K+V of a tile landed
   uint64_t* empty = bars + STAGES;       // [STAGES] stage consumed by PV
-  uint64_t* s_full = bars + 2 * STAGES;  // [2] S tile in TMEM
-  uint64_t* s_free = s_full + 2;         // [2] S tile read by softmax
-  uint64_t* p_full = s_free + 2;         // P in smem (+ O rescaled)
-  uint64_t* o_done = p_full + 1;         // PV committed
-  uint64_t* q_full = o_done + 1;         // Q in smem
+  uint64_t* s_full = bars + 2 * STAGES;  // [2 pipes] S tile in TMEM
+  uint64_t* s_free = s_full + 2;         // [2] S read by softmax
+  uint64_t* p_full = s_free + 2;         // [2] P in smem (+ O rescaled)
+  uint64_t* o_done = p_full + 2;         // [2] PV committed
+  uint64_t* q_full = o_done + 2;         // Q in smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
   const AttnItem it = a.items[blockIdx.x];
@@ -184,13 +189,13 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&s_free[b], 4);
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(&s_full[p], 1);
+      mbar_init(&s_free[p], 4);
+      mbar_init(&p_full[p], 4);
+      mbar_init(&o_done[p], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
-    mbar_init(q_full, 4);
+    mbar_init(q_full, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -207,8 +212,7 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
     // ---------------- TMA producer (whole warp: lane i resolves page i) ----------------
     if (n_tiles > 0) {
       const int ppt = BN / S;  // pages per tile
-      // pool row of the K slice of logical page lp (out of bounds -> TMA zero fill)
-      auto row_of = [&](uint64_t lp) -> int {
+      auto row_of = [&](uint64_t lp) -> int {  // pool row of a logical page's K slice
         if (lp < user_pages) {
           const uint32_t page = a.pages[R.pages_off + uint32_t(lp)];
           return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
@@ -217,11 +221,10 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
           const uint32_t page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
           return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
         }
-        return -int(S) * 4;
+        return -int(S) * 4;  // out of bounds -> TMA zero fill
       };
       const uint64_t lp_base = k_lo / S;
-      // lanes cover 32 consecutive pages; refreshed every 32/ppt tiles
-      int rows_cache = row_of(lp_base + lane);
+      int rows_cache = row_of(lp_base + lane);  // 32 consecutive pages per refresh
       int cache_tile0 = 0;
       for (int t = 0; t < n_tiles; ++t) {
         const int st = t % STAGES;
@@ -250,65 +253,67 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer: non-blocking event loop over both pipelines ----------------
     if (lane == 0 && n_tiles > 0) {
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
           (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-      const uint32_t q_addr = s32(sQ), p_addr = s32(sP);
+      const uint32_t q_addr = s32(sQ);
       mbar_wait(q_full, 0);
       tc_after();
-      auto issue_s = [&](int t) {
-        const int st = t % STAGES, sb = t & 1;
-        mbar_wait(&full[st], (t / STAGES) & 1);
-        if (t >= 2) mbar_wait(&s_free[sb], ((t / 2) - 1) & 1);
-        tc_after();
-        const uint32_t k_addr = s32(sKV + st * STAGE_BYTES);
+      int next_s = 0, next_pv = 0;
+      while (next_pv < n_tiles) {
+        bool progressed = false;
+        // PV first: it frees a K/V stage and unblocks the owning softmax warpgroup
+        if (next_pv < next_s) {
+          const int t = next_pv, p = t & 1, u = t >> 1, st = t % STAGES;
+          if (mbar_ready(&p_full[p], u & 1)) {
+            tc_after();
+            const uint32_t p_addr = s32(sP + p * P_BYTES);
+            const uint32_t v_addr = s32(sKV + st * STAGE_BYTES + KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          mma_f16(tmem + S_COL0 + sb * BN, sdesc(q_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024),
-                  sdesc(k_addr + (k / 4) * KBLK + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
-        mma_commit(&s_full[sb]);
-      };
-      issue_s(0);
-      int s_issued = 1;  // S tiles issued so far
-      for (int t = 0; t < n_tiles; ++t) {
-        // S(t+1) overlaps softmax(t) when its K tile has landed; PV(t) must not wait for it
-        if (s_issued == t + 1 && t + 1 < n_tiles && mbar_ready(&full[(t + 1) % STAGES], ((t + 1) / STAGES) & 1)) {
-          issue_s(t + 1);
-          ++s_issued;
+            for (int k = 0; k < BN / 16; ++k) {
+              const uint64_t pa = sdesc(p_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024);
+              const uint64_t vb = sdesc(v_addr + k * 2048, KBLK, 1024);  // MN-major V, LBO = KBLK
+              mma_f16(tmem + p * PIPE_COLS + BN, pa, vb, idesc_o, (u > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&o_done[p]);
+            mma_commit(&empty[st]);
+            ++next_pv;
+            progressed = true;
+          }
         }
-        const int st = t % STAGES;
-        mbar_wait(p_full, t & 1);
-        tc_after();
-        const uint32_t v_addr = s32(sKV + st * STAGE_BYTES + KV_BYTES);
+        if (next_s < n_tiles && next_s < next_pv + 2) {  // at most one S ahead per pipeline
+          const int t = next_s, p = t & 1, u = t >> 1, st = t % STAGES;
+          if (mbar_ready(&full[st], (t / STAGES) & 1) && (u == 0 || mbar_ready(&s_free[p], (u - 1) & 1))) {
+            tc_after();
+            const uint32_t k_addr = s32(sKV + st * STAGE_BYTES);
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) {
-          // A = P (K-major, keys contiguous): block k/4, +32 B per step
-          const uint64_t pa = sdesc(p_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024);
-          // B = V (MN-major): 16 keys = 2 row groups of 8 -> +2048 B; dim blocks LBO = KBLK
-          const uint64_t vb = sdesc(v_addr + k * 2048, KBLK, 1024);
-          mma_f16(tmem + O_COL, pa, vb, idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < D / 16; ++k)
+              mma_f16(tmem + p * PIPE_COLS, sdesc(q_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024),
+                      sdesc(k_addr + (k / 4) * KBLK + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
+            mma_commit(&s_full[p]);
+            ++next_s;
+            progressed = true;
+          }
         }
-        mma_commit(o_done);
-        mma_commit(&empty[st]);
-        if (s_issued == t + 1 && t + 1 < n_tiles) {
-          issue_s(t + 1);
-          ++s_issued;
-        }
+        if (!progressed) __nanosleep(20);
       }
     }
   } else if (warp >= 4) {
-    // ---------------- softmax warpgroup ----------------
-    const uint32_t r = threadIdx.x - 128;  // query row within the tile == TMEM lane
-    const uint32_t lane_base = (32u * (warp - 4)) << 16;
-    // Q row -> smem (SW128 K-major); rows past the request read finite data or zeros
+    // ---------------- softmax warpgroups ----------------
+    const uint32_t p = (warp - 4) / 4;          // pipeline
+    const uint32_t r = (threadIdx.x - 128) % 128;  // query row == TMEM lane
+    const uint32_t lane_base = (32u * (warp % 4)) << 16;
+    const uint32_t s_col = p * PIPE_COLS, o_col = p * PIPE_COLS + BN;
+    uint8_t* myP = sP + p * P_BYTES;
+    // Q row -> smem (SW128 K-major); each warpgroup writes half of the row's blocks
     {
       const uint32_t qi = q0 + r;
       const bool ok = qi < R.n_q;
       const uint4* src = reinterpret_cast<const uint4*>(a.q + size_t(R.q_row0 + (ok ? qi : 0)) * g.d + h * D);
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
+      for (int c = p; c < D / 8; c += 2) {
         uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(sQ + (c / 8) * QBLK + sw128(r, c % 8)) = v;
       }
@@ -321,18 +326,17 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
     const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
     const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
     float m_ref = -INFINITY, l_run = 0.f;
-    for (int t = 0; t < n_tiles; ++t) {
-      const int sb = t & 1;
-      mbar_wait(&s_full[sb], (t / 2) & 1);
+    int u = 0;
+    for (int t = p; t < n_tiles; t += 2, ++u) {
+      mbar_wait(&s_full[p], u & 1);
       tc_after();
       float s[BN];
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tmem + lane_base + S_COL0 + sb * BN + c * 32, s + c * 32);
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tmem + lane_base + s_col + c * 32, s + c * 32);
       tmem_wait_ld();
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[sb]);
-      // mask (two half-open ranges relative to the tile) + scale, base 2
+      if (lane == 0) mbar_arrive(&s_free[p]);
       const uint64_t kb = k_lo + uint64_t(t) * BN;
       const int cu = int(u_end > kb ? (u_end - kb < uint64_t(BN) ? u_end - kb : uint64_t(BN)) : 0);
       const int c_lo = int(KAp > kb ? (KAp - kb < uint64_t(BN) ? KAp - kb : uint64_t(BN)) : 0);
@@ -352,10 +356,8 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
           mx = fmaxf(mx, s[c]);
         }
       }
-      // lazy rescale: keep the reference max unless the new max exceeds it by
-      // more than 2^8 (p <= 256 stays exact enough in fp32/bf16)
       float alpha = 1.f;
-      if (mx > m_ref + kRescale) {
+      if (mx > m_ref + kRescale) {  // lazy rescale: p <= 2^8 between rescales
         alpha = m_ref == -INFINITY ? 0.f : ex2(m_ref - mx);
         m_ref = mx;
       }
@@ -367,24 +369,22 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         rs += s[c];
       }
       l_run = l_run * alpha + rs;
-      // PV of the previous tile must be done before O is rescaled / P is overwritten
-      if (t > 0) {
-        mbar_wait(o_done, (t - 1) & 1);
+      if (u > 0) {  // this pipeline's previous PV must finish before O / P are touched
+        mbar_wait(&o_done[p], (u - 1) & 1);
         tc_after();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             float o[32];
-            tmem_ld32(tmem + lane_base + O_COL + c * 32, o);
+            tmem_ld32(tmem + lane_base + o_col + c * 32, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st32(tmem + lane_base + O_COL + c * 32, o);
+            tmem_st32(tmem + lane_base + o_col + c * 32, o);
           }
           tmem_wait_st();
         }
       }
-      // P row -> smem, bf16, SW128 K-major (blocks of 64 keys)
 #pragma unroll
       for (int c = 0; c < BN / 8; ++c) {
         uint4 v;
@@ -392,26 +392,27 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
         v.y = pack2(s[c * 8 + 2], s[c * 8 + 3]);
         v.z = pack2(s[c * 8 + 4], s[c * 8 + 5]);
         v.w = pack2(s[c * 8 + 6], s[c * 8 + 7]);
-        *reinterpret_cast<uint4*>(sP + (c / 8) * QBLK + sw128(r, c % 8)) = v;
+        *reinterpret_cast<uint4*>(myP + (c / 8) * QBLK + sw128(r, c % 8)) = v;
       }
       fence_async_smem();
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[p]);
     }
-    // epilogue: O / l and lse (base 2) for the split
+    // epilogue: this pipeline's O / l and lse (base 2) as partial 2*split + p
     const uint32_t qi = q0 + r;
-    if (n_tiles > 0) {
-      mbar_wait(o_done, (n_tiles - 1) & 1);
+    if (u > 0) {
+      mbar_wait(&o_done[p], (u - 1) & 1);
       tc_after();
     }
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    float* dst = a.part_o + (size_t(R.part_base) + size_t(it.split) * R.n_q + qi) * g.d + h * D;
+    const size_t prow = size_t(R.part_base) + (size_t(it.split) * 2 + p) * R.n_q + qi;
+    float* dst = a.part_o + prow * g.d + h * D;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       float o[32];
-      if (n_tiles > 0) {
-        tmem_ld32(tmem + lane_base + O_COL + c * 32, o);
+      if (u > 0) {
+        tmem_ld32(tmem + lane_base + o_col + c * 32, o);
         tmem_wait_ld();
       } else {
 #pragma unroll
@@ -423,9 +424,7 @@ __global__ void __launch_bounds__(256, 1) attn_tc_kernel(const __grid_constant__
           *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
       }
     }
-    if (qi < q_end)
-      a.part_lse[(size_t(R.part_base) + size_t(it.split) * R.n_q + qi) * g.H + h] =
-          l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
+    if (qi < q_end) a.part_lse[prow * g.H + h] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
   }
   tc_before();
   __syncthreads();
@@ -463,13 +462,13 @@ int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
 
 template <int D>
 static void launch_tc_d(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {
-  constexpr size_t smem = 1024 + (D / 64) * BM * 128 + (BN / 64) * BM * 128 + STAGES * 2 * (D / 64) * BN * 128 + 256;
+  constexpr size_t smem = 1024 + (D / 64) * BM * 128 + 2 * (BN / 64) * BM * 128 + STAGES * 2 * (D / 64) * BN * 128 + 256;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     set = true;
   }
-  attn_tc_kernel<D><<<a.n_items, 256, smem, s>>>(map, a);
+  attn_tc_kernel<D><<<a.n_items, 384, smem, s>>>(map, a);
 }
 
 void launch_attention_tc(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {

@@ -358,6 +358,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
 
   // ---- rows, attention work, metadata sizes ----
   std::vector<ReqDev> rd(n);
+  key_splits_.assign(n, 1);
   uint32_t rows = 0, part_rows = 0, max_hist = 0, n_items = 0, ncand_total = 0;
   // tcgen05 path: 128-row query tiles over the page-padded logical key space,
   // 1024-key splits; mma.sync path (head_dim < 64): 512-key splits over positions
@@ -383,10 +384,13 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     const uint64_t KA = x.start + x.n_hist;
     const uint64_t T = tc ? (KA + S - 1) / S * S + x.n_cand : x.start + x.n_q;
     x.split_keys = x.n_q <= 256 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 128, 0xFFFFFF00ull));
-    x.n_splits = uint32_t((T + x.split_keys - 1) / x.split_keys);
+    const uint32_t key_splits = uint32_t((T + x.split_keys - 1) / x.split_keys);
+    key_splits_[r] = key_splits;
+    // the tcgen05 kernel writes two partials per key split (one per softmax pipeline)
+    x.n_splits = tc ? 2 * key_splits : key_splits;
     x.part_base = part_rows;
     part_rows += x.n_splits * x.n_q;
-    n_items += H * ((x.n_q + bq - 1) / bq) * x.n_splits;
+    n_items += H * ((x.n_q + bq - 1) / bq) * key_splits;
     rows += x.n_q;
     ncand_total += x.n_cand;
     max_hist = std::max(max_hist, x.n_hist);
@@ -460,7 +464,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     h_last[r] = x.q_row0 + x.n_q - 1;
     for (uint32_t h = 0; h < H; ++h)
       for (uint32_t qt = 0; qt < (x.n_q + bq - 1) / bq; ++qt)
-        for (uint32_t s = 0; s < x.n_splits; ++s) h_items[it++] = AttnItem{r, h, qt, s};
+        for (uint32_t s = 0; s < key_splits_[r]; ++s) h_items[it++] = AttnItem{r, h, qt, s};
     last_nc_[r] = x.n_cand;
     for (uint32_t c = 0; c < x.n_cand; ++c) {
       const uint32_t id = value_ ? w.tokens[R.tok_off + x.n_hist + c] : 0;

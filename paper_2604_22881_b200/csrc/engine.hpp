@@ -86,6 +86,7 @@ class Engine {
   float* w_ln_ = nullptr;
   uint32_t staging_slots_ = 0;
   bool use_tc_ = false;          // tcgen05 attention (head_dim 64/128)
+  std::vector<uint32_t> key_splits_;  // per request of the batch being enqueued
   alignas(64) CUtensorMap pool_map_{};
   const void* pool_map_ptr_ = nullptr;
 

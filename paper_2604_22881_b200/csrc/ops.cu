@@ -1,5 +1,7 @@
 // Raw device ops of the C-ABI (kernel-level parity tests and integrations that
 // own their buffers): chunk scatter/gather and single-request paged attention.
+#include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "kernels.cuh"
@@ -56,6 +58,19 @@ static int chunk_op(bool to_pool, void* pool, void* staging, const uint32_t* d_p
   return finish(e);
 }
 
+// out = merge of the two pipeline partials (log-sum-exp weights, base 2)
+__global__ void merge2_kernel(float* out, const float* part, const float* lse, uint32_t n_q, uint32_t H,
+                              uint32_t D) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x, d = H * D;
+  if (idx >= n_q * d) return;
+  const uint32_t i = idx / d, j = idx % d, h = j / D;
+  const float l0 = lse[size_t(i) * H + h], l1 = lse[(size_t(n_q) + i) * H + h];
+  const float m = fmaxf(l0, l1);
+  const float w0 = l0 == -INFINITY ? 0.f : exp2f(l0 - m), w1 = l1 == -INFINITY ? 0.f : exp2f(l1 - m);
+  const float den = w0 + w1;
+  out[idx] = den > 0.f ? (w0 * part[idx] + w1 * part[size_t(n_q) * d + idx]) / den : 0.f;
+}
+
 extern "C" {
 
 int mtkv_op_scatter_chunks(void* pool, const void* staging, const uint32_t* d_page_ids, uint32_t n_chunks,
@@ -87,10 +102,10 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   r.pages_off = 0;
   r.n_pages = uint32_t((n_keys + g.S - 1) / g.S);
   r.part_base = 0;
-  r.n_splits = 1;
-  r.split_keys = 0xFFFFFFFFu;
+  r.split_keys = 0xFFFFFF00u;
   const char* force = std::getenv("MTKV_ATTN");
   const bool tc = attn_tc_supported(g) && !(force && std::string(force) == "mma");
+  r.n_splits = tc ? 2 : 1;  // the tcgen05 kernel emits one partial per softmax pipeline
   const uint32_t bq = (tc || n_q > 64) ? 128 : 64;
   const uint32_t qtiles = (n_q + bq - 1) / bq, n_items = g.H * qtiles;
   AttnItem* hi = new AttnItem[n_items];
@@ -98,12 +113,14 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   for (uint32_t h = 0; h < g.H; ++h)
     for (uint32_t t = 0; t < qtiles; ++t) hi[k++] = AttnItem{0, h, t, 0};
   char* buf = nullptr;
-  const size_t bytes = 256 + n_items * sizeof(AttnItem) + size_t(n_q) * g.H * sizeof(float);
+  const size_t part_bytes = tc ? size_t(2) * n_q * g.d * sizeof(float) : 0;
+  const size_t bytes = 256 + n_items * sizeof(AttnItem) + size_t(2) * n_q * g.H * sizeof(float) + part_bytes;
   cudaError_t e = cudaMallocAsync((void**)&buf, bytes, s);
   if (e != cudaSuccess) { delete[] hi; return finish(e); }
   ReqDev* dr = reinterpret_cast<ReqDev*>(buf);
   AttnItem* di = reinterpret_cast<AttnItem*>(buf + 256);
   float* lse = reinterpret_cast<float*>(buf + 256 + n_items * sizeof(AttnItem));
+  float* part = tc ? lse + size_t(2) * n_q * g.H : nullptr;
   e = cudaMemcpyAsync(dr, &r, sizeof(r), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(di, hi, n_items * sizeof(AttnItem), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -115,7 +132,7 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   a.reqs = dr;
   a.items = di;
   a.n_items = n_items;
-  a.part_o = out;
+  a.part_o = tc ? part : out;
   a.part_lse = lse;
   a.g = g;
   a.layer = layer;
@@ -130,6 +147,7 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
         return MTKV_ERROR;
       }
       launch_attention_tc(map, a, s);
+      merge2_kernel<<<(n_q * g.d + 255) / 256, 256, 0, s>>>(out, part, lse, n_q, g.H, g.D);
     } else {
       launch_attention(a, s);
     }
