@@ -125,6 +125,17 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATTN_TR(kind, t)                                                                  \
+  do {                                                                                    \
+    if (a.trace && blockIdx.x < kTraceCtas && (t) < kTraceTiles)                          \
+      a.trace[((size_t)blockIdx.x * kTraceKinds + (kind)) * kTraceTiles + (t)] = gtime(); \
+  } while (0)
+
 struct Smem {
   static constexpr uint32_t kBlock = BM * 128;  // one 128-row x 64-elem bf16 block = 16 KB
 };
@@ -171,6 +182,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const PoolGeom& g = a.g;
   const uint32_t S = g.S, h = it.head;
+  if (threadIdx.x == 0) ATTN_TR(5, 0);
 
   // logical key space: user keys [0, KA) padded to KAp, then candidates
   const uint64_t KA = R.start + R.n_hist;
@@ -207,6 +219,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) ATTN_TR(5, 1);
 
   if (warp == 0) {
     // ---------------- TMA producer (whole warp: lane i resolves page i) ----------------
@@ -234,6 +247,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
         }
         if (lane == 0) {
           if (t >= STAGES) mbar_wait(&empty[st], ((t / STAGES) - 1) & 1);
+          ATTN_TR(0, t);
           mbar_expect_tx(&full[st], STAGE_BYTES);
         }
         __syncwarp();
@@ -279,6 +293,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
             }
             mma_commit(&o_done[p]);
             mma_commit(&empty[st]);
+            ATTN_TR(2, t);
             ++next_pv;
             progressed = true;
           }
@@ -293,6 +308,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
               mma_f16(tmem + p * PIPE_COLS, sdesc(q_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024),
                       sdesc(k_addr + (k / 4) * KBLK + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
             mma_commit(&s_full[p]);
+            ATTN_TR(1, t);
             ++next_s;
             progressed = true;
           }
@@ -330,6 +346,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
     for (int t = p; t < n_tiles; t += 2, ++u) {
       mbar_wait(&s_full[p], u & 1);
       tc_after();
+      if (threadIdx.x % 128 == 0) ATTN_TR(3, t);
       float s[BN];
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tmem_ld32(tmem + lane_base + s_col + c * 32, s + c * 32);
@@ -398,6 +415,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[p]);
+      if (threadIdx.x % 128 == 0) ATTN_TR(4, t);
     }
     // epilogue: this pipeline's O / l and lse (base 2) as partial 2*split + p
     const uint32_t qi = q0 + r;
@@ -425,6 +443,7 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
       }
     }
     if (qi < q_end) a.part_lse[prow * g.H + h] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
+    if (threadIdx.x == 128) ATTN_TR(5, 2);
   }
   tc_before();
   __syncthreads();

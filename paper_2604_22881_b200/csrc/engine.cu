@@ -77,7 +77,7 @@ Engine::~Engine() {
     refill_.join();
   }
   if (comp_) cudaDeviceSynchronize();
-  DevBuf* bufs[] = {&pool_, &staging_[0], &staging_[1], &offload_, &meta_, &x_, &x2_, &u_, &q_,
+  DevBuf* bufs[] = {&trace_, &pool_, &staging_[0], &staging_[1], &offload_, &meta_, &x_, &x2_, &u_, &q_,
                     &mid_, &part_o_, &part_lse_, &logits_, &scores_};
   for (DevBuf* b : bufs) b->release();
   for (void* p : {(void*)w_embed_, (void*)w_in_, (void*)w1_, (void*)w2_, (void*)w_out_, (void*)w_ln_})
@@ -585,6 +585,14 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
       aa.g = g_; aa.layer = l; aa.bq = bq; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
+      if (tc && trace_path_ && l == 0) {  // MTKV_ATTN_TRACE: per-CTA timelines of layer 0
+        if (!trace_.p && trace_.ensure(size_t(kTraceCtas) * kTraceKinds * kTraceTiles * 8)) {
+          err = "engine: trace alloc";
+          return MTKV_ERROR;
+        }
+        CK(cudaMemsetAsync(trace_.p, 0, trace_.bytes, comp_));
+        aa.trace = static_cast<unsigned long long*>(trace_.p);
+      }
       if (tc) {
         if (pool_map_ptr_ != pool_.p) {
           if (make_pool_map(&pool_map_, pool_.p, g_)) { err = "engine: cuTensorMapEncodeTiled failed"; return MTKV_ERROR; }
@@ -790,6 +798,15 @@ double Engine::last_batch_ms() {
 
 double Engine::last_attention_ms(uint32_t* n) {
   if (n) *n = attn_launches_last_;
+  if (trace_path_ && trace_.p && last_slot_ >= 0) {
+    cudaEventSynchronize(ev_done_[last_slot_]);
+    std::vector<unsigned long long> h(trace_.bytes / 8);
+    cudaMemcpy(h.data(), trace_.p, trace_.bytes, cudaMemcpyDeviceToHost);
+    if (FILE* f = std::fopen(trace_path_, "wb")) {
+      std::fwrite(h.data(), 8, h.size(), f);
+      std::fclose(f);
+    }
+  }
   if (last_slot_ < 0 || !opt_.profile || ev_attn_.empty()) return 0;
   cudaEventSynchronize(ev_done_[last_slot_]);
   double tot = 0;

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -87,6 +89,8 @@ class Engine {
   uint32_t staging_slots_ = 0;
   bool use_tc_ = false;          // tcgen05 attention (head_dim 64/128)
   std::vector<uint32_t> key_splits_;  // per request of the batch being enqueued
+  const char* trace_path_ = std::getenv("MTKV_ATTN_TRACE");
+  DevBuf trace_;
   alignas(64) CUtensorMap pool_map_{};
   const void* pool_map_ptr_ = nullptr;
 
