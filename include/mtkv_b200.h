@@ -153,6 +153,14 @@ int mtkv_engine_last_logits(mtkv_engine* e, float* out, uint32_t cap_rows);
 /* rank_candidates (model.cpp:199) for each request of the last batch: writes
  * the candidate ids in descending logit order (stable) into out (concatenated) */
 int mtkv_engine_last_rankings(mtkv_engine* e, uint32_t* out, uint64_t cap);
+/* Pipelined serving: rankings of an earlier batch, identified by its ticket
+ * (0-based index among successfully submitted batches), while later batches are
+ * still in flight; the last 4 submitted batches stay readable. Blocks until that
+ * batch has completed. The reference returns each batch's results from
+ * Engine::process_batch (sim.hpp:332); this splits submit and read-back so the
+ * host can enqueue batch i+1's onload before reading batch i. */
+int mtkv_engine_batch_rankings(mtkv_engine* e, uint64_t ticket, uint32_t* out, uint64_t cap);
+uint64_t mtkv_engine_batches_submitted(const mtkv_engine* e);
 /* check_conservation (sim.cpp:60), tag backend: reads back the whole device
  * pool and host store and verifies every resident token's identity */
 int mtkv_engine_check_conservation(mtkv_engine* e);

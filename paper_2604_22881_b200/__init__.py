@@ -124,7 +124,8 @@ EXPORTED_SYMBOLS = [
     "mtkv_planner_create", "mtkv_planner_destroy", "mtkv_planner_process_batch", "mtkv_planner_drain",
     "mtkv_engine_create", "mtkv_engine_destroy", "mtkv_engine_process_batch", "mtkv_engine_run",
     "mtkv_engine_drain", "mtkv_engine_synchronize", "mtkv_engine_last_logits",
-    "mtkv_engine_last_rankings", "mtkv_engine_check_conservation", "mtkv_engine_read_user_kv",
+    "mtkv_engine_last_rankings", "mtkv_engine_batch_rankings", "mtkv_engine_batches_submitted",
+    "mtkv_engine_check_conservation", "mtkv_engine_read_user_kv",
     "mtkv_engine_last_batch_ms", "mtkv_engine_last_attention_ms", "mtkv_engine_kernel_launches",
     "mtkv_engine_set_profile",
     "mtkv_report", "mtkv_last_plans", "mtkv_last_evictions", "mtkv_known_users", "mtkv_user_state",
@@ -168,6 +169,8 @@ def lib():
         "mtkv_engine_synchronize": (C.c_int, [vp]),
         "mtkv_engine_last_logits": (C.c_int, [vp, C.POINTER(C.c_float), u32]),
         "mtkv_engine_last_rankings": (C.c_int, [vp, u32p, u64]),
+        "mtkv_engine_batch_rankings": (C.c_int, [vp, u64, u32p, u64]),
+        "mtkv_engine_batches_submitted": (u64, [vp]),
         "mtkv_engine_check_conservation": (C.c_int, [vp]),
         "mtkv_engine_read_user_kv": (C.c_int64, [vp, u32, u32, C.POINTER(C.c_uint16),
                                                  C.POINTER(C.c_uint16), u64]),
@@ -345,6 +348,9 @@ class RequestBatch:
             else:
                 q.candidate_count = int(r.get("nc", 1))
 
+    def candidate_counts(self) -> list[int]:
+        return [self.arr[i].candidate_count for i in range(self.n)]
+
 
 def batchify(trace: Sequence[dict], batch_size: int):
     """workload.cpp:247 batchify."""
@@ -453,6 +459,14 @@ class Planner(_ManagerView):
         _check(lib().mtkv_planner_drain(self._h))
 
 
+class Ticket:
+    """Handle of a submitted batch (Engine.submit)."""
+    __slots__ = ("batch", "counts")
+
+    def __init__(self, batch: int, counts: list[int]):
+        self.batch, self.counts = batch, counts
+
+
 class Engine(_ManagerView):
     """sim.hpp:110 Engine<B> with the data plane on a B200 (sm_100a kernels)."""
     _is_engine = 1
@@ -487,6 +501,26 @@ class Engine(_ManagerView):
     def process_batch(self, batch, packed: RequestBatch | None = None) -> None:
         rb = packed or RequestBatch(batch)
         _check(lib().mtkv_engine_process_batch(self._h, rb.arr, rb.n))
+
+    def submit(self, batch=None, packed: RequestBatch | None = None) -> "Ticket":
+        """Pipelined serving: enqueue a batch and return a ticket for its results
+        (read them with rankings(ticket) while later batches are in flight)."""
+        rb = packed or RequestBatch(batch)
+        _check(lib().mtkv_engine_process_batch(self._h, rb.arr, rb.n))
+        return Ticket(int(lib().mtkv_engine_batches_submitted(self._h)) - 1, rb.candidate_counts())
+
+    def rankings(self, ticket: "Ticket") -> list[list[int]]:
+        """rank_candidates (model.cpp:199) of every request of the ticket's batch."""
+        tot = sum(ticket.counts)
+        out = np.zeros(max(tot, 1), dtype=np.uint32)
+        n = lib().mtkv_engine_batch_rankings(self._h, ticket.batch, out.ctypes.data_as(C.POINTER(C.c_uint32)), tot)
+        if n < 0:
+            raise Error(_err())
+        res, o = [], 0
+        for c in ticket.counts:
+            res.append(out[o:o + c].tolist())
+            o += c
+        return res
 
     def run(self, trace: Sequence[dict]) -> dict:
         """sim.hpp:135 run(): batchify, process, drain, report."""

@@ -1,21 +1,30 @@
 // Incremental prefix-reuse attention on the 5th-gen tensor cores (sm_100a).
 //
-// One CTA = (request, head, 128-row query tile, key split). Warp roles:
-//   warp 0      TMA producer: page-granular cp.async.bulk.tensor loads of K and V
-//               straight out of the paged pool (no gather pass), 2-stage ring
-//   warp 1      MMA issuer (one elected thread): S = Q K^T and O += P V with
-//               tcgen05.mma kind::f16, accumulators in TMEM
-//   warp 2      TMEM allocator (512 columns: S double buffer + O)
-//   warps 4..7  softmax warpgroup: thread r owns query row r; tcgen05.ld of its
-//               S row, mask, online softmax (base 2), P -> smem (bf16, SW128),
-//               conditional O rescale in TMEM, epilogue O/l + lse to HBM
+// Persistent kernel: one CTA per SM streams a contiguous, equal-length range
+// of 64-key tiles (attn_plan.cpp); the range is a list of pieces, each a key
+// range of one (request, head, 128-row query tile) segment. The K/V rings keep
+// streaming across piece boundaries, so an SM never idles on a prologue.
+// Warp roles (384 threads):
+//   warp 0      K producer: page-granular cp.async.bulk.tensor loads of K tiles
+//               straight out of the paged pool (no gather pass), NK-stage ring
+//   warp 3      V producer: same for V, NV-stage ring (V stays until PV, K is
+//               released as soon as S = Q K^T has been issued)
+//   warp 2      TMEM allocator, then Q loader (TMA, double-buffered per piece)
+//   warp 1      MMA issuer (one elected thread): S = Q K^T (A, B in smem) and
+//               O += P V (A = P in TMEM, B = V in smem) with tcgen05.mma
+//               kind::f16, fp32 accumulators in TMEM
+//   warps 4..11 two softmax pipelines (tiles of a piece alternate between
+//               them): thread r owns query row r (= TMEM lane r): tcgen05.ld of
+//               its S row, mask, online softmax in base 2, P -> TMEM (bf16x2,
+//               tcgen05.st), lazy O rescale, epilogue O/l + lse per piece
 // Logical key space: the user's keys [0, KA) padded to a page boundary, then
 // the request's candidate keys (their own scratch pages), so every page-sized
 // slice of a tile is one TMA box. Keys past the end load as zeros (TMA OOB).
 //
-// Operand layouts (canonical UMMA, 128-byte swizzle, 1024-B aligned):
-//   Q, P, K : K-major  [rows][64-elem blocks], SBO = 1024 B, +32 B per K=16 step
-//   V       : MN-major [keys][64-dim blocks],  SBO = 1024 B, LBO = 16 KB
+// Shared-memory operand layouts (canonical UMMA, 128-byte swizzle):
+//   Q, K : K-major  [rows][64-elem blocks], SBO = 1024 B, +32 B per K=16 step
+//   V    : MN-major [keys][64-dim blocks],  SBO = 1024 B, LBO = one block
+// TMEM columns per pipeline: S (64 fp32) | P (32 x bf16x2) | O (D fp32).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,7 +38,6 @@ namespace tc {
 
 constexpr int BM = 128;   // query rows per tile (TMEM lanes)
 constexpr int BN = 64;    // keys per tile
-constexpr int STAGES = 4; // K+V ring depth
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -80,6 +88,13 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b,
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -136,83 +151,90 @@ __device__ __forceinline__ unsigned long long gtime() {
       a.trace[((size_t)blockIdx.x * kTraceKinds + (kind)) * kTraceTiles + (t)] = gtime(); \
   } while (0)
 
-struct Smem {
-  static constexpr uint32_t kBlock = BM * 128;  // one 128-row x 64-elem bf16 block = 16 KB
-};
-
 }  // namespace tc
 
 using namespace tc;
 
-// Two softmax pipelines per CTA: warpgroup p in {0,1} owns key tiles t with
-// t % 2 == p, its own S and O accumulators in TMEM and its own P buffer, and
-// writes its result as partial (2*split + p); the split-K merge in
-// gate_norm_kernel combines them. While one warpgroup runs softmax the tensor
-// core works on the other pipeline's S / PV, so neither unit waits on the other.
+
 template <int D>
-__global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, AttnArgs a) {
-  constexpr int NB = D / 64;                            // 64-element column blocks of Q/K/V
-  constexpr uint32_t QBLK = BM * 128;                   // Q/P block: 128 rows x 128 B
-  constexpr uint32_t KBLK = BN * 128;                   // K/V block: BN rows x 128 B
-  constexpr uint32_t Q_BYTES = NB * QBLK;
-  constexpr uint32_t P_BYTES = (BN / 64) * QBLK;        // 128 rows x BN keys (per pipeline)
-  constexpr uint32_t KV_BYTES = NB * KBLK;              // BN keys x D (K or V)
-  constexpr uint32_t STAGE_BYTES = 2 * KV_BYTES;
-  constexpr uint32_t PIPE_COLS = BN + D;                // S + O per pipeline
-  constexpr uint32_t TMEM_COLS = 2 * PIPE_COLS <= 256 ? 256 : 512;
-  constexpr float kRescale = 8.f;                       // lazy rescale threshold (log2 units)
+struct TcCfg {
+  static constexpr int NB = D / 64;                      // 64-element column blocks of Q/K/V
+  static constexpr uint32_t QBLK = BM * 128;             // 128 rows x 128 B
+  static constexpr uint32_t Q_BYTES = NB * QBLK;
+  static constexpr uint32_t KBLK = BN * 128;             // 64 keys x 128 B
+  static constexpr uint32_t T_BYTES = NB * KBLK;         // one K (or V) tile
+  static constexpr int NK = D == 128 ? 5 : 8;            // K ring stages
+  static constexpr int NV = D == 128 ? 5 : 8;            // V ring stages
+  static constexpr uint32_t S_COL = 0, P_COL = BN, O_COL = BN + BN / 2, PIPE = BN + BN / 2 + D;
+  static constexpr uint32_t TMEM_COLS = 2 * PIPE <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + 2 * Q_BYTES + size_t(NK + NV) * T_BYTES + 256;
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+struct TileCursor {  // walks a CTA's pieces tile by tile
+  uint32_t pc, end, t, lo, hi, j, g, k, c0, c1;  // c0/c1: tiles issued per pipeline
+  __device__ void init(const AttnArgs& a, uint32_t b, uint32_t e) {
+    pc = b; end = e; g = 0; k = 0; j = 0; c0 = c1 = 0;
+    load(a);
+  }
+  __device__ void load(const AttnArgs& a) {
+    if (pc < end) { const AttnPiece P = a.pieces[pc]; lo = P.lo; hi = P.hi; t = lo; }
+  }
+  __device__ void next(const AttnArgs& a) {
+    if (j & 1) ++c1; else ++c0;
+    ++g; ++t; ++j;
+    if (t == hi) { ++pc; ++k; j = 0; load(a); }
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map, AttnArgs a) {
+  using C = TcCfg<D>;
+  constexpr int NB = C::NB, NK = C::NK, NV = C::NV;
+  constexpr uint32_t QBLK = C::QBLK, KBLK = C::KBLK, T_BYTES = C::T_BYTES, Q_BYTES = C::Q_BYTES;
+  constexpr float kRescale = 8.f;  // lazy rescale threshold (log2 units): p <= 2^8 between rescales
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sP = sQ + Q_BYTES;                 // [2] pipelines
-  uint8_t* sKV = sP + 2 * P_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;                 // [STAGES] K+V of a tile landed
-  uint64_t* empty = bars + STAGES;       // [STAGES] stage consumed by PV
-  uint64_t* s_full = bars + 2 * STAGES;  // [2 pipes] S tile in TMEM
-  uint64_t* s_free = s_full + 2;         // [2] S read by softmax
-  uint64_t* p_full = s_free + 2;         // [2] P in smem (+ O rescaled)
-  uint64_t* o_done = p_full + 2;         // [2] PV committed
-  uint64_t* q_full = o_done + 2;         // Q in smem
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+  uint8_t* sQ = smem;                          // [2] Q buffers
+  uint8_t* sK = sQ + 2 * Q_BYTES;              // [NK] K tiles
+  uint8_t* sV = sK + NK * T_BYTES;             // [NV] V tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NV * T_BYTES);
+  uint64_t* full_k = bars;
+  uint64_t* empty_k = full_k + NK;
+  uint64_t* full_v = empty_k + NK;
+  uint64_t* empty_v = full_v + NV;
+  uint64_t* s_full = empty_v + NV;  // [2 pipes] S tile in TMEM
+  uint64_t* s_free = s_full + 2;    // [2] S read by softmax
+  uint64_t* p_full = s_free + 2;    // [2] P in TMEM (+ O rescaled)
+  uint64_t* o_done = p_full + 2;    // [2] PV completed
+  uint64_t* q_full = o_done + 2;    // [2] Q buffer landed
+  uint64_t* q_empty = q_full + 2;   // [2] Q buffer's S MMAs completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 2);
 
-  const AttnItem it = a.items[blockIdx.x];
-  const ReqDev R = a.reqs[it.req];
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
   const PoolGeom& g = a.g;
-  const uint32_t S = g.S, h = it.head;
+  const uint32_t S = g.S;
   if (threadIdx.x == 0) ATTN_TR(5, 0);
 
-  // logical key space: user keys [0, KA) padded to KAp, then candidates
-  const uint64_t KA = R.start + R.n_hist;
-  const uint64_t KAp = (KA + S - 1) / S * S;
-  const uint32_t user_pages = uint32_t(KAp / S);
-  const uint32_t q0 = it.qtile * BM;
-  const uint32_t q_end = min(R.n_q, q0 + BM);
-  const uint64_t pos_last = R.start + q_end - 1;
-  const uint64_t k_vis = pos_last >= KA ? KAp + (pos_last - KA + 1) : pos_last + 1;
-  const uint64_t k_lo = uint64_t(it.split) * R.split_keys;
-  const uint64_t k_hi = min(k_vis, k_lo + uint64_t(R.split_keys));
-  const int n_tiles = k_hi > k_lo ? int((k_hi - k_lo + BN - 1) / BN) : 0;
-
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 1); }
+    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 1); }
     for (int p = 0; p < 2; ++p) {
       mbar_init(&s_full[p], 1);
       mbar_init(&s_free[p], 4);
       mbar_init(&p_full[p], 4);
       mbar_init(&o_done[p], 1);
+      mbar_init(&q_full[p], 1);
+      mbar_init(&q_empty[p], 1);
     }
-    mbar_init(q_full, 8);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tmem_slot)),
-                 "n"(TMEM_COLS));
+                 "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_before();
@@ -221,95 +243,116 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) ATTN_TR(5, 1);
 
-  if (warp == 0) {
-    // ---------------- TMA producer (whole warp: lane i resolves page i) ----------------
-    if (n_tiles > 0) {
-      const int ppt = BN / S;  // pages per tile
+  if (warp == 0 || warp == 3) {
+    // ---------------- K / V producers (whole warp: lane i resolves page i) ----------------
+    const bool isv = warp == 3;
+    uint64_t* full = isv ? full_v : full_k;
+    uint64_t* empty = isv ? empty_v : empty_k;
+    uint8_t* ring = isv ? sV : sK;
+    const uint32_t NS = isv ? NV : NK;
+    const uint32_t ppt = BN / S;  // pages per tile
+    uint32_t gt = 0;
+    for (uint32_t pc = pb; pc < pe; ++pc) {
+      const AttnPiece P = a.pieces[pc];
+      const AttnSeg sg = a.segs[P.seg];
+      const ReqDev R = a.reqs[sg.req];
+      const uint64_t KA = R.start + R.n_hist;
+      const uint32_t user_pages = uint32_t((KA + S - 1) / S);
+      const uint32_t col = sg.head * D;
       auto row_of = [&](uint64_t lp) -> int {  // pool row of a logical page's K slice
-        if (lp < user_pages) {
-          const uint32_t page = a.pages[R.pages_off + uint32_t(lp)];
-          return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
-        }
-        if (lp - user_pages < R.n_scratch && (lp - user_pages) * S < R.n_cand) {
-          const uint32_t page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
-          return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
-        }
-        return -int(S) * 4;  // out of bounds -> TMA zero fill
+        uint32_t page;
+        if (lp < user_pages) page = a.pages[R.pages_off + uint32_t(lp)];
+        else if (lp - user_pages < R.n_scratch && (lp - user_pages) * S < R.n_cand)
+          page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
+        else return -int(S) * 4;  // out of bounds -> TMA zero fill
+        return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
       };
-      const uint64_t lp_base = k_lo / S;
-      int rows_cache = row_of(lp_base + lane);  // 32 consecutive pages per refresh
-      int cache_tile0 = 0;
-      for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % STAGES;
-        if ((t - cache_tile0) * ppt >= 32) {
-          cache_tile0 = t;
-          rows_cache = row_of(lp_base + uint64_t(t) * ppt + lane);
+      uint32_t cache_t0 = P.lo;
+      int rows_cache = row_of(uint64_t(P.lo) * ppt + lane);  // 32 consecutive pages per refresh
+      for (uint32_t t = P.lo; t < P.hi; ++t, ++gt) {
+        const uint32_t st = gt % NS;
+        if ((t - cache_t0) * ppt >= 32) {
+          cache_t0 = t;
+          rows_cache = row_of(uint64_t(t) * ppt + lane);
         }
         if (lane == 0) {
-          if (t >= STAGES) mbar_wait(&empty[st], ((t / STAGES) - 1) & 1);
-          ATTN_TR(0, t);
-          mbar_expect_tx(&full[st], STAGE_BYTES);
+          if (gt >= NS) mbar_wait(&empty[st], ((gt / NS) - 1) & 1);
+          if (!isv) ATTN_TR(0, gt);
+          mbar_expect_tx(&full[st], T_BYTES);
         }
         __syncwarp();
-        uint8_t* kdst = sKV + st * STAGE_BYTES;
-        uint8_t* vdst = kdst + KV_BYTES;
-        for (int i = 0; i < ppt; ++i) {
-          const int row_k = __shfl_sync(0xffffffffu, rows_cache, (t - cache_tile0) * ppt + i);
-          const int row_v = row_k >= 0 ? row_k + int(S) : row_k;
+        uint8_t* dst = ring + st * T_BYTES;
+        for (uint32_t i = 0; i < ppt; ++i) {
+          int row = __shfl_sync(0xffffffffu, rows_cache, (t - cache_t0) * ppt + i);
+          if (isv && row >= 0) row += int(S);
           if (lane == 0) {
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              tma_load_2d(kdst + b * KBLK + i * S * 128, &pool_map, int(h * D + 64 * b), row_k, &full[st]);
-              tma_load_2d(vdst + b * KBLK + i * S * 128, &pool_map, int(h * D + 64 * b), row_v, &full[st]);
-            }
+            for (int b = 0; b < NB; ++b)
+              tma_load_2d(dst + b * KBLK + i * S * 128, &pool_map, int(col + 64 * b), row, &full[st]);
           }
         }
       }
     }
+  } else if (warp == 2) {
+    // ---------------- Q loader: one TMA box per 64-column block, double-buffered ----------------
+    if (lane == 0) {
+      uint32_t k = 0;
+      for (uint32_t pc = pb; pc < pe; ++pc, ++k) {
+        const AttnPiece P = a.pieces[pc];
+        const AttnSeg sg = a.segs[P.seg];
+        const ReqDev R = a.reqs[sg.req];
+        const uint32_t qb = k & 1;
+        if (k >= 2) mbar_wait(&q_empty[qb], ((k >> 1) - 1) & 1);
+        mbar_expect_tx(&q_full[qb], Q_BYTES);
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          tma_load_2d(sQ + qb * Q_BYTES + b * QBLK, &q_map, int(sg.head * D + 64 * b), int(R.q_row0 + sg.qtile * BM),
+                      &q_full[qb]);
+      }
+    }
   } else if (warp == 1) {
     // ---------------- MMA issuer: non-blocking event loop over both pipelines ----------------
-    if (lane == 0 && n_tiles > 0) {
+    if (lane == 0 && pe > pb) {
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
           (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-      const uint32_t q_addr = s32(sQ);
-      mbar_wait(q_full, 0);
-      tc_after();
-      int next_s = 0, next_pv = 0;
-      while (next_pv < n_tiles) {
+      TileCursor cs, cv;
+      cs.init(a, pb, pe);
+      cv.init(a, pb, pe);
+      while (cv.pc < pe) {
         bool progressed = false;
-        // PV first: it frees a K/V stage and unblocks the owning softmax warpgroup
-        if (next_pv < next_s) {
-          const int t = next_pv, p = t & 1, u = t >> 1, st = t % STAGES;
-          if (mbar_ready(&p_full[p], u & 1)) {
+        // PV first: it frees a V stage and unblocks the owning softmax pipeline
+        if (cv.g < cs.g) {
+          const uint32_t p = cv.j & 1, u = p ? cv.c1 : cv.c0, stv = cv.g % NV;
+          if (mbar_ready(&p_full[p], u & 1) && mbar_ready(&full_v[stv], (cv.g / NV) & 1)) {
             tc_after();
-            const uint32_t p_addr = s32(sP + p * P_BYTES);
-            const uint32_t v_addr = s32(sKV + st * STAGE_BYTES + KV_BYTES);
+            const uint32_t v_addr = s32(sV + stv * T_BYTES);
 #pragma unroll
-            for (int k = 0; k < BN / 16; ++k) {
-              const uint64_t pa = sdesc(p_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024);
-              const uint64_t vb = sdesc(v_addr + k * 2048, KBLK, 1024);  // MN-major V, LBO = KBLK
-              mma_f16(tmem + p * PIPE_COLS + BN, pa, vb, idesc_o, (u > 0 || k > 0) ? 1u : 0u);
-            }
+            for (int kk = 0; kk < BN / 16; ++kk)
+              mma_ts(tmem + p * C::PIPE + C::O_COL, tmem + p * C::PIPE + C::P_COL + kk * 8,
+                     sdesc(v_addr + kk * 2048, KBLK, 1024), idesc_o, (cv.j >= 2 || kk > 0) ? 1u : 0u);
             mma_commit(&o_done[p]);
-            mma_commit(&empty[st]);
-            ATTN_TR(2, t);
-            ++next_pv;
+            mma_commit(&empty_v[stv]);
+            ATTN_TR(2, cv.g);
+            cv.next(a);
             progressed = true;
           }
         }
-        if (next_s < n_tiles && next_s < next_pv + 2) {  // at most one S ahead per pipeline
-          const int t = next_s, p = t & 1, u = t >> 1, st = t % STAGES;
-          if (mbar_ready(&full[st], (t / STAGES) & 1) && (u == 0 || mbar_ready(&s_free[p], (u - 1) & 1))) {
+        if (cs.pc < pe && cs.g < cv.g + 2) {  // at most one S ahead per pipeline
+          const uint32_t p = cs.j & 1, u = p ? cs.c1 : cs.c0, stk = cs.g % NK, qb = cs.k & 1;
+          if (mbar_ready(&full_k[stk], (cs.g / NK) & 1) && (u == 0 || mbar_ready(&s_free[p], (u - 1) & 1)) &&
+              (cs.j != 0 || mbar_ready(&q_full[qb], (cs.k >> 1) & 1))) {
             tc_after();
-            const uint32_t k_addr = s32(sKV + st * STAGE_BYTES);
+            const uint32_t q_addr = s32(sQ + qb * Q_BYTES), k_addr = s32(sK + stk * T_BYTES);
 #pragma unroll
-            for (int k = 0; k < D / 16; ++k)
-              mma_f16(tmem + p * PIPE_COLS, sdesc(q_addr + (k / 4) * QBLK + (k % 4) * 32, 16, 1024),
-                      sdesc(k_addr + (k / 4) * KBLK + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_f16(tmem + p * C::PIPE + C::S_COL, sdesc(q_addr + (kk / 4) * QBLK + (kk % 4) * 32, 16, 1024),
+                      sdesc(k_addr + (kk / 4) * KBLK + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
             mma_commit(&s_full[p]);
-            ATTN_TR(1, t);
-            ++next_s;
+            mma_commit(&empty_k[stk]);
+            if (cs.t + 1 == cs.hi) mma_commit(&q_empty[qb]);  // last S of the piece: Q buffer reusable
+            ATTN_TR(1, cs.g);
+            cs.next(a);
             progressed = true;
           }
         }
@@ -317,138 +360,130 @@ __global__ void __launch_bounds__(384, 1) attn_tc_kernel(const __grid_constant__
       }
     }
   } else if (warp >= 4) {
-    // ---------------- softmax warpgroups ----------------
-    const uint32_t p = (warp - 4) / 4;          // pipeline
+    // ---------------- softmax pipelines ----------------
+    const uint32_t p = (warp - 4) / 4;             // pipeline
     const uint32_t r = (threadIdx.x - 128) % 128;  // query row == TMEM lane
     const uint32_t lane_base = (32u * (warp % 4)) << 16;
-    const uint32_t s_col = p * PIPE_COLS, o_col = p * PIPE_COLS + BN;
-    uint8_t* myP = sP + p * P_BYTES;
-    // Q row -> smem (SW128 K-major); each warpgroup writes half of the row's blocks
-    {
-      const uint32_t qi = q0 + r;
-      const bool ok = qi < R.n_q;
-      const uint4* src = reinterpret_cast<const uint4*>(a.q + size_t(R.q_row0 + (ok ? qi : 0)) * g.d + h * D);
-#pragma unroll
-      for (int c = p; c < D / 8; c += 2) {
-        uint4 v = ok ? src[c] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sQ + (c / 8) * QBLK + sw128(r, c % 8)) = v;
-      }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
-    }
-    const uint64_t pos_r = R.start + q0 + r;
-    // valid keys of this row: user keys [0, u_end), candidate keys [KAp, c_end)
-    const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
-    const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
-    float m_ref = -INFINITY, l_run = 0.f;
-    int u = 0;
-    for (int t = p; t < n_tiles; t += 2, ++u) {
-      mbar_wait(&s_full[p], u & 1);
-      tc_after();
-      if (threadIdx.x % 128 == 0) ATTN_TR(3, t);
-      float s[BN];
-#pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tmem + lane_base + s_col + c * 32, s + c * 32);
-      tmem_wait_ld();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[p]);
-      const uint64_t kb = k_lo + uint64_t(t) * BN;
-      const int cu = int(u_end > kb ? (u_end - kb < uint64_t(BN) ? u_end - kb : uint64_t(BN)) : 0);
-      const int c_lo = int(KAp > kb ? (KAp - kb < uint64_t(BN) ? KAp - kb : uint64_t(BN)) : 0);
-      const int c_hi = int(c_end > kb ? (c_end - kb < uint64_t(BN) ? c_end - kb : uint64_t(BN)) : 0);
-      float mx = -INFINITY;
-      if (cu == BN) {
-#pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          s[c] *= a.scale_log2;
-          mx = fmaxf(mx, s[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          const bool ok = c < cu || (c >= c_lo && c < c_hi);
-          s[c] = ok ? s[c] * a.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[c]);
-        }
-      }
-      float alpha = 1.f;
-      if (mx > m_ref + kRescale) {  // lazy rescale: p <= 2^8 between rescales
-        alpha = m_ref == -INFINITY ? 0.f : ex2(m_ref - mx);
-        m_ref = mx;
-      }
-      const float mref = m_ref == -INFINITY ? 0.f : m_ref;
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < BN; ++c) {
-        s[c] = ex2(s[c] - mref);
-        rs += s[c];
-      }
-      l_run = l_run * alpha + rs;
-      if (u > 0) {  // this pipeline's previous PV must finish before O / P are touched
-        mbar_wait(&o_done[p], (u - 1) & 1);
+    const uint32_t s_col = tmem + lane_base + p * C::PIPE + C::S_COL;
+    const uint32_t p_col = tmem + lane_base + p * C::PIPE + C::P_COL;
+    const uint32_t o_col = tmem + lane_base + p * C::PIPE + C::O_COL;
+    uint32_t u = 0;  // tiles this pipeline has processed (barrier phases)
+    for (uint32_t pc = pb; pc < pe; ++pc) {
+      const AttnPiece P = a.pieces[pc];
+      const AttnSeg sg = a.segs[P.seg];
+      const ReqDev R = a.reqs[sg.req];
+      const uint64_t KA = R.start + R.n_hist;
+      const uint64_t KAp = (KA + S - 1) / S * S;
+      const uint32_t q0 = sg.qtile * BM;
+      const uint32_t q_end = min(R.n_q, q0 + BM);
+      const uint64_t pos_last = R.start + q_end - 1;
+      const uint64_t k_vis = pos_last >= KA ? KAp + (pos_last - KA + 1) : pos_last + 1;
+      const uint64_t k_hi = min(k_vis, uint64_t(P.hi) * BN);
+      const uint64_t pos_r = R.start + q0 + r;
+      // valid keys of this row: user keys [0, u_end), candidate keys [KAp, c_end)
+      const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
+      const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
+      float m_ref = -INFINITY, l_run = 0.f;
+      uint32_t mine = 0;
+      for (uint32_t t = P.lo + p; t < P.hi; t += 2, ++u, ++mine) {
+        mbar_wait(&s_full[p], u & 1);
         tc_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        if (threadIdx.x % 128 == 0) ATTN_TR(3, u * 2 + p);
+        float s[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_col + c * 32, s + c * 32);
+        tmem_wait_ld();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[p]);
+        const uint64_t kb = uint64_t(t) * BN;
+        const int cu = int(u_end > kb ? (u_end - kb < uint64_t(BN) ? u_end - kb : uint64_t(BN)) : 0);
+        const int c_lo = int(KAp > kb ? (KAp - kb < uint64_t(BN) ? KAp - kb : uint64_t(BN)) : 0);
+        const int c_hi = int(c_end > kb ? (c_end - kb < uint64_t(BN) ? c_end - kb : uint64_t(BN)) : 0);
+        float mx = -INFINITY;
+        if (cu == BN) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) {
+            s[c] *= a.scale_log2;
+            mx = fmaxf(mx, s[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) {
+            const bool ok = c < cu || (c >= c_lo && c < c_hi);
+            s[c] = ok ? s[c] * a.scale_log2 : -INFINITY;
+            mx = fmaxf(mx, s[c]);
+          }
+        }
+        float alpha = 1.f;
+        if (mx > m_ref + kRescale) {
+          alpha = m_ref == -INFINITY ? 0.f : ex2(m_ref - mx);
+          m_ref = mx;
+        }
+        const float mref = m_ref == -INFINITY ? 0.f : m_ref;
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          s[c] = ex2(s[c] - mref);
+          rs += s[c];
+        }
+        l_run = l_run * alpha + rs;
+        if (u > 0) {  // this pipeline's previous PV must finish before P / O are touched
+          mbar_wait(&o_done[p], (u - 1) & 1);
+          tc_after();
+        }
+        if (mine > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             float o[32];
-            tmem_ld32(tmem + lane_base + o_col + c * 32, o);
+            tmem_ld32(o_col + c * 32, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st32(tmem + lane_base + o_col + c * 32, o);
+            tmem_st32(o_col + c * 32, o);
           }
-          tmem_wait_st();
+        }
+        uint32_t pk[BN / 2];
+#pragma unroll
+        for (int c = 0; c < BN / 2; ++c) pk[c] = pack2(s[2 * c], s[2 * c + 1]);
+        tmem_st32(p_col, reinterpret_cast<const float*>(pk));
+        tmem_wait_st();
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[p]);
+        if (threadIdx.x % 128 == 0) ATTN_TR(4, u * 2 + p);
+      }
+      // epilogue: this pipeline's O / l and lse (base 2) into slot part + p
+      const uint32_t qi = q0 + r;
+      if (mine > 0) {
+        mbar_wait(&o_done[p], (u - 1) & 1);
+        tc_after();
+      }
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const size_t prow = size_t(P.part + p) * BM + r;
+      float* dst = a.part_o + prow * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float o[32];
+        if (mine > 0) {
+          tmem_ld32(o_col + c * 32, o);
+          tmem_wait_ld();
+        }
+        if (qi < q_end && mine > 0) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
         }
       }
-#pragma unroll
-      for (int c = 0; c < BN / 8; ++c) {
-        uint4 v;
-        v.x = pack2(s[c * 8 + 0], s[c * 8 + 1]);
-        v.y = pack2(s[c * 8 + 2], s[c * 8 + 3]);
-        v.z = pack2(s[c * 8 + 4], s[c * 8 + 5]);
-        v.w = pack2(s[c * 8 + 6], s[c * 8 + 7]);
-        *reinterpret_cast<uint4*>(myP + (c / 8) * QBLK + sw128(r, c % 8)) = v;
-      }
-      fence_async_smem();
+      if (qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
       tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[p]);
-      if (threadIdx.x % 128 == 0) ATTN_TR(4, t);
     }
-    // epilogue: this pipeline's O / l and lse (base 2) as partial 2*split + p
-    const uint32_t qi = q0 + r;
-    if (u > 0) {
-      mbar_wait(&o_done[p], (u - 1) & 1);
-      tc_after();
-    }
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    const size_t prow = size_t(R.part_base) + (size_t(it.split) * 2 + p) * R.n_q + qi;
-    float* dst = a.part_o + prow * g.d + h * D;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      float o[32];
-      if (u > 0) {
-        tmem_ld32(tmem + lane_base + o_col + c * 32, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = 0.f;
-      }
-      if (qi < q_end) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
-      }
-    }
-    if (qi < q_end) a.part_lse[prow * g.H + h] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
     if (threadIdx.x == 128) ATTN_TR(5, 2);
   }
   tc_before();
   __syncthreads();
   tc_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
 // ------------------------------------------------------------------ host ---
@@ -462,38 +497,53 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool attn_tc_supported(const PoolGeom& g) {
-  return (g.D == 64 || g.D == 128) && g.S >= 8 && g.S <= 128 && (128 % g.S) == 0;
+  return (g.D == 64 || g.D == 128) && g.S >= 8 && g.S <= BN && (BN % g.S) == 0;
 }
 
-int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
-  const cuuint64_t rows = cuuint64_t(g.L) * g.num_pages * 2 * g.S;
-  const cuuint64_t dims[2] = {g.d, rows};
-  const cuuint64_t strides[1] = {cuuint64_t(g.d) * 2};
-  const cuuint32_t box[2] = {64, g.S};
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 1;
+}
+
+static int encode_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  const cuuint32_t box[2] = {64, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   auto fn = encode_fn();
   if (!fn) return -1;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-template <int D>
-static void launch_tc_d(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {
-  constexpr size_t smem = 1024 + (D / 64) * BM * 128 + 2 * (BN / 64) * BM * 128 + STAGES * 2 * (D / 64) * BN * 128 + 256;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    set = true;
-  }
-  attn_tc_kernel<D><<<a.n_items, 384, smem, s>>>(map, a);
+// pool viewed as rows of d elements: [L * num_pages * 2 * S][d], box = 64 cols x one page
+int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
+  return encode_2d(map, pool, g.d, uint64_t(g.L) * g.num_pages * 2 * g.S, g.S);
 }
 
-void launch_attention_tc(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s) {
+// fresh-row queries [rows][d], box = 64 cols x 128 rows (rows past the buffer load as zeros)
+int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g) {
+  return encode_2d(map, q, g.d, rows, BM);
+}
+
+template <int D>
+static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
+    set = true;
+  }
+  attn_tc_kernel<D><<<a.n_items, 384, TcCfg<D>::SMEM, s>>>(pool_map, q_map, a);
+}
+
+void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
-  if (a.g.D == 64) launch_tc_d<64>(map, a, s);
-  else launch_tc_d<128>(map, a, s);
+  if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, a, s);
+  else launch_tc_d<128>(pool_map, q_map, a, s);
 }
 
 }  // namespace mtkv_b200

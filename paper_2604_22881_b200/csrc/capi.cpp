@@ -233,6 +233,14 @@ int mtkv_engine_last_rankings(mtkv_engine* e, uint32_t* out, uint64_t cap) {
   return !err.empty() ? (fail(MTKV_ERROR, err), -1) : rc;
 }
 
+int mtkv_engine_batch_rankings(mtkv_engine* e, uint64_t ticket, uint32_t* out, uint64_t cap) {
+  std::string err;
+  const int rc = e->e.batch_rankings(ticket, out, cap, err);
+  return !err.empty() ? (fail(MTKV_ERROR, err), -1) : rc;
+}
+
+uint64_t mtkv_engine_batches_submitted(const mtkv_engine* e) { return e->e.batches_submitted(); }
+
 int mtkv_engine_check_conservation(mtkv_engine* e) {
   std::string err;
   const int rc = e->e.check_conservation(err);

@@ -169,6 +169,7 @@ int Engine::init(std::string& err) {
     const char* f = std::getenv("MTKV_ATTN");
     use_tc_ = attn_tc_supported(g_) && !(f && std::string(f) == "mma");
   }
+  n_sm_ = num_sms();
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
@@ -358,19 +359,12 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
 
   // ---- rows, attention work, metadata sizes ----
   std::vector<ReqDev> rd(n);
-  key_splits_.assign(n, 1);
-  uint32_t rows = 0, part_rows = 0, max_hist = 0, n_items = 0, ncand_total = 0;
-  // tcgen05 path: 128-row query tiles over the page-padded logical key space,
-  // 1024-key splits; mma.sync path (head_dim < 64): 512-key splits over positions
+  uint32_t rows = 0, max_hist = 0, ncand_total = 0;
   const bool tc = use_tc_;
-  const uint32_t kSplitKeys = tc ? 1024 : 512;
-  uint32_t max_q = 0;
-  for (uint32_t r = 0; r < n; ++r)
-    max_q = std::max(max_q, w.reqs[r].n_hist + w.reqs[r].plan.num_candidates);
-  const uint32_t bq = (tc || max_q > 64) ? 128 : 64;  // one tile covers typical fresh rows (Δ + candidates)
   for (uint32_t r = 0; r < n; ++r) {
     const ReqWork& R = w.reqs[r];
     ReqDev& x = rd[r];
+    x = ReqDev{};
     x.q_row0 = rows;
     x.n_hist = R.n_hist;
     x.n_cand = R.plan.num_candidates;
@@ -381,20 +375,15 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     x.scratch_off = recompute_ ? t_soff[r] : R.scratch_off;
     x.n_scratch = recompute_ ? t_ns[r] : R.n_scratch;
     x.user = R.plan.user;
-    const uint64_t KA = x.start + x.n_hist;
-    const uint64_t T = tc ? (KA + S - 1) / S * S + x.n_cand : x.start + x.n_q;
-    x.split_keys = x.n_q <= 256 ? kSplitKeys : uint32_t(std::min<uint64_t>(T + 128, 0xFFFFFF00ull));
-    const uint32_t key_splits = uint32_t((T + x.split_keys - 1) / x.split_keys);
-    key_splits_[r] = key_splits;
-    // the tcgen05 kernel writes two partials per key split (one per softmax pipeline)
-    x.n_splits = tc ? 2 * key_splits : key_splits;
-    x.part_base = part_rows;
-    part_rows += x.n_splits * x.n_q;
-    n_items += H * ((x.n_q + bq - 1) / bq) * key_splits;
     rows += x.n_q;
     ncand_total += x.n_cand;
     max_hist = std::max(max_hist, x.n_hist);
   }
+  if (value_) plan_attention(rd.data(), n, g_, tc, tc ? uint32_t(n_sm_) : 0, plan_);
+  const uint32_t bq = plan_.bm;
+  const uint32_t n_segs = value_ ? uint32_t(plan_.segs.size()) : 0;
+  const uint32_t n_items = value_ ? (tc ? plan_.n_ctas() : uint32_t(plan_.items.size())) : 0;
+  const uint32_t n_pieces = value_ && tc ? uint32_t(plan_.pieces.size()) : 0;
   const uint32_t n_on = uint32_t(w.onloads.size()), n_off = uint32_t(w.offloads.size());
 
   size_t need = 0;
@@ -404,7 +393,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   need = align16(need + rows * sizeof(uint64_t));      // kv_off
   need = align16(need + rows * sizeof(uint32_t));      // row_req
   need = align16(need + n * sizeof(uint32_t));         // last_row
-  need = align16(need + n_items * sizeof(AttnItem));
+  need = align16(need + n_segs * sizeof(AttnSeg));
+  need = align16(need + (tc ? 0 : n_items) * sizeof(AttnItem));
+  need = align16(need + n_pieces * sizeof(AttnPiece));
+  need = align16(need + (tc ? n_items + 1 : 0) * sizeof(uint32_t));
   need = align16(need + (n_on + n_off) * sizeof(ChunkWork));
   need = align16(need + 2 * ncand_total * sizeof(uint32_t));
   if (meta_host_bytes_[k] < need) {
@@ -428,8 +420,14 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   uint32_t* h_rr = carve<uint32_t>(hb, off, rows);
   const size_t o_last = off;
   uint32_t* h_last = carve<uint32_t>(hb, off, n);
+  const size_t o_segs = off;
+  AttnSeg* h_segs = carve<AttnSeg>(hb, off, n_segs);
   const size_t o_items = off;
-  AttnItem* h_items = carve<AttnItem>(hb, off, n_items);
+  AttnItem* h_items = carve<AttnItem>(hb, off, tc ? 0 : n_items);
+  const size_t o_pieces = off;
+  AttnPiece* h_pieces = carve<AttnPiece>(hb, off, n_pieces);
+  const size_t o_ctaoff = off;
+  uint32_t* h_ctaoff = carve<uint32_t>(hb, off, tc ? n_items + 1 : 0);
   const size_t o_chunks = off;
   ChunkWork* h_chunks = carve<ChunkWork>(hb, off, n_on + n_off);
   const size_t o_cand = off;
@@ -439,9 +437,16 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
 
   std::memcpy(h_req, rd.data(), n * sizeof(ReqDev));
   if (!pages.empty()) std::memcpy(h_pages, pages.data(), pages.size() * sizeof(uint32_t));
-  last_cands_.clear();
-  last_nc_.assign(n, 0);
-  uint32_t it = 0, cj = 0;
+  std::vector<uint32_t>& cands_k = slot_cands_[k];
+  std::vector<uint32_t>& nc_k = slot_nc_[k];
+  cands_k.clear();
+  nc_k.assign(n, 0);
+  slot_batch_[k] = int64_t(batch_no_);
+  uint32_t cj = 0;
+  if (n_segs) std::memcpy(h_segs, plan_.segs.data(), n_segs * sizeof(AttnSeg));
+  if (!tc && n_items) std::memcpy(h_items, plan_.items.data(), n_items * sizeof(AttnItem));
+  if (n_pieces) std::memcpy(h_pieces, plan_.pieces.data(), n_pieces * sizeof(AttnPiece));
+  if (tc && n_items) std::memcpy(h_ctaoff, plan_.cta_off.data(), (n_items + 1) * sizeof(uint32_t));
   for (uint32_t r = 0; r < n; ++r) {
     const ReqDev& x = rd[r];
     const ReqWork& R = w.reqs[r];
@@ -462,15 +467,12 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       h_kv[row] = (uint64_t(page) * 2 * S + slot) * d;
     }
     h_last[r] = x.q_row0 + x.n_q - 1;
-    for (uint32_t h = 0; h < H; ++h)
-      for (uint32_t qt = 0; qt < (x.n_q + bq - 1) / bq; ++qt)
-        for (uint32_t s = 0; s < key_splits_[r]; ++s) h_items[it++] = AttnItem{r, h, qt, s};
-    last_nc_[r] = x.n_cand;
+    nc_k[r] = x.n_cand;
     for (uint32_t c = 0; c < x.n_cand; ++c) {
       const uint32_t id = value_ ? w.tokens[R.tok_off + x.n_hist + c] : 0;
       h_creq[cj] = r;
       h_cid[cj] = id;
-      last_cands_.push_back(id);
+      cands_k.push_back(id);
       ++cj;
     }
   }
@@ -536,7 +538,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   const uint64_t* d_kv = reinterpret_cast<const uint64_t*>(db + o_kv);
   const uint32_t* d_rr = reinterpret_cast<const uint32_t*>(db + o_rr);
   const uint32_t* d_last = reinterpret_cast<const uint32_t*>(db + o_last);
+  const AttnSeg* d_segs = reinterpret_cast<const AttnSeg*>(db + o_segs);
   const AttnItem* d_items = reinterpret_cast<const AttnItem*>(db + o_items);
+  const AttnPiece* d_pieces = reinterpret_cast<const AttnPiece*>(db + o_pieces);
+  const uint32_t* d_ctaoff = reinterpret_cast<const uint32_t*>(db + o_ctaoff);
   const ChunkWork* d_chunks = reinterpret_cast<const ChunkWork*>(db + o_chunks);
   const uint32_t* d_creq = reinterpret_cast<const uint32_t*>(db + o_cand);
   const uint32_t* d_cid = d_creq + ncand_total;
@@ -553,8 +558,8 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   if (value_) {
     const size_t rb = size_t(rows) * d * sizeof(__nv_bfloat16);
     if (x_.ensure(rb) || x2_.ensure(rb) || u_.ensure(rb) || q_.ensure(rb) || mid_.ensure(rb) ||
-        part_o_.ensure(size_t(part_rows) * d * sizeof(float)) ||
-        part_lse_.ensure(size_t(part_rows) * H * sizeof(float)) ||
+        part_o_.ensure(size_t(plan_.n_slots) * bq * g_.D * sizeof(float)) ||
+        part_lse_.ensure(size_t(plan_.n_slots) * bq * sizeof(float)) ||
         logits_.ensure(size_t(n) * V * sizeof(float)) || scores_.ensure(size_t(ncand_total) * sizeof(float))) {
       err = "engine: workspace alloc";
       return MTKV_ERROR;
@@ -581,7 +586,8 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       ga.layer_base = size_t(l) * g_.num_pages * 2 * S * d; ga.d = d; ga.kv_stride = S * d;
       launch_gemm(ga, comp_);
       AttnArgs aa{};
-      aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.items = d_items; aa.n_items = n_items;
+      aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.segs = d_segs; aa.items = d_items;
+      aa.n_items = n_items; aa.pieces = d_pieces; aa.cta_off = d_ctaoff;
       aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
       aa.g = g_; aa.layer = l; aa.bq = bq; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
@@ -594,18 +600,27 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
         aa.trace = static_cast<unsigned long long*>(trace_.p);
       }
       if (tc) {
-        if (pool_map_ptr_ != pool_.p) {
+        if (pool_map_ptr_ != pool_.p || pool_map_pages_ != g_.num_pages) {
           if (make_pool_map(&pool_map_, pool_.p, g_)) { err = "engine: cuTensorMapEncodeTiled failed"; return MTKV_ERROR; }
           pool_map_ptr_ = pool_.p;
+          pool_map_pages_ = g_.num_pages;
         }
-        launch_attention_tc(pool_map_, aa, comp_);
+        if (q_map_ptr_ != q_.p || q_map_bytes_ != q_.bytes) {
+          if (make_q_map(&q_map_, q_.p, q_.bytes / (size_t(d) * sizeof(__nv_bfloat16)), g_)) {
+            err = "engine: cuTensorMapEncodeTiled (queries) failed";
+            return MTKV_ERROR;
+          }
+          q_map_ptr_ = q_.p;
+          q_map_bytes_ = q_.bytes;
+        }
+        launch_attention_tc(pool_map_, q_map_, aa, comp_);
       } else {
         launch_attention(aa, comp_);
       }
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l + 1], comp_));
       ++attn_launches_last_;
       GateArgs gn{};
-      gn.part_o = aa.part_o; gn.part_lse = aa.part_lse; gn.u = U; gn.ln_scale = w_ln_ + size_t(l) * d;
+      gn.part_o = aa.part_o; gn.part_lse = aa.part_lse; gn.segs = d_segs; gn.bm = bq; gn.u = U; gn.ln_scale = w_ln_ + size_t(l) * d;
       gn.row_req = d_rr; gn.reqs = d_req; gn.out = X2; gn.rows = rows; gn.H = H; gn.D = g_.D;
       launch_gate_norm(gn, comp_);
       GemmArgs m1{};
@@ -713,19 +728,32 @@ int Engine::last_logits(float* out, uint32_t cap_rows, std::string& err) {
 }
 
 int Engine::last_rankings(uint32_t* out, uint64_t cap, std::string& err) {
-  if (!value_) { err = "rankings: tag backend has no model"; return MTKV_ERROR; }
   if (last_slot_ < 0) return 0;
-  CK(cudaEventSynchronize(ev_done_[last_slot_]));
-  const float* sc = scores_host_[last_slot_];
+  return batch_rankings(batch_no_ - 1, out, cap, err);
+}
+
+int Engine::batch_rankings(uint64_t ticket, uint32_t* out, uint64_t cap, std::string& err) {
+  if (!value_) { err = "rankings: tag backend has no model"; return MTKV_ERROR; }
+  const int k = int(ticket % kRing);
+  if (ticket >= batch_no_ || slot_batch_[k] != int64_t(ticket)) {
+    err = "rankings: results of batch " + std::to_string(ticket) + " are not available (only the last " +
+          std::to_string(kRing) + " submitted batches are kept)";
+    return MTKV_ERROR;
+  }
+  CK(cudaEventSynchronize(ev_done_[k]));
+  const float* sc = scores_host_[k];
+  const std::vector<uint32_t>& cands = slot_cands_[k];
+  const std::vector<uint32_t>& nc = slot_nc_[k];
   uint64_t o = 0;
   size_t base = 0;
-  for (uint32_t r = 0; r < last_n_; ++r) {
-    std::vector<uint32_t> idx(last_nc_[r]);
-    for (uint32_t i = 0; i < last_nc_[r]; ++i) idx[i] = i;
+  std::vector<uint32_t> idx;
+  for (uint32_t r = 0; r < nc.size(); ++r) {
+    idx.resize(nc[r]);
+    for (uint32_t i = 0; i < nc[r]; ++i) idx[i] = i;
     std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return sc[base + a] > sc[base + b]; });
     for (uint32_t i : idx)
-      if (o < cap) out[o++] = last_cands_[base + i];
-    base += last_nc_[r];
+      if (o < cap) out[o++] = cands[base + i];
+    base += nc[r];
   }
   return int(o);
 }

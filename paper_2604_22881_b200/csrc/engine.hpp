@@ -46,6 +46,10 @@ class Engine {
   int synchronize(std::string& err);
   int last_logits(float* out, uint32_t cap_rows, std::string& err);
   int last_rankings(uint32_t* out, uint64_t cap, std::string& err);
+  // rankings of an earlier batch (ticket = 0-based submission index) while later
+  // batches are in flight; valid for the last kRing submitted batches
+  int batch_rankings(uint64_t ticket, uint32_t* out, uint64_t cap, std::string& err);
+  uint64_t batches_submitted() const { return batch_no_; }
   int check_conservation(std::string& err);
   int64_t read_user_kv(uint32_t user, uint32_t layer, uint16_t* k, uint16_t* v, uint64_t cap,
                        std::string& err);
@@ -88,11 +92,16 @@ class Engine {
   float* w_ln_ = nullptr;
   uint32_t staging_slots_ = 0;
   bool use_tc_ = false;          // tcgen05 attention (head_dim 64/128)
-  std::vector<uint32_t> key_splits_;  // per request of the batch being enqueued
+  int n_sm_ = 1;                 // persistent attention CTAs
+  AttnPlan plan_;                // attention plan of the batch being enqueued
   const char* trace_path_ = std::getenv("MTKV_ATTN_TRACE");
   DevBuf trace_;
   alignas(64) CUtensorMap pool_map_{};
+  alignas(64) CUtensorMap q_map_{};
   const void* pool_map_ptr_ = nullptr;
+  uint32_t pool_map_pages_ = 0;
+  const void* q_map_ptr_ = nullptr;
+  size_t q_map_bytes_ = 0;
 
   // pinned host memory: slabs -> per-user extents -> chunks
   static constexpr size_t kSpareSlabs = 2;
@@ -119,7 +128,9 @@ class Engine {
 
   // last batch bookkeeping for logits / rankings
   uint32_t last_n_ = 0;
-  std::vector<uint32_t> last_cands_, last_nc_;
+  // per ring slot: candidate ids and counts of the batch whose scores it holds
+  std::vector<uint32_t> slot_cands_[kRing], slot_nc_[kRing];
+  int64_t slot_batch_[kRing] = {-1, -1, -1, -1};
   uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0, onload_chunks_ = 0, offload_chunks_ = 0;
 };
 

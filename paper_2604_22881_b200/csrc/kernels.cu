@@ -409,16 +409,17 @@ __global__ void __launch_bounds__(NW * 32) attn_kernel(AttnArgs a) {
   for (int r = 0; r < 2; ++r) {
     const uint32_t qi = q0 + warp * 16 + gq + r * 8;
     if (qi >= q_end) continue;
-    const size_t prow = (size_t)R.part_base + (size_t)it.split * R.n_q + qi;
+    const AttnSeg& sg = a.segs[R.seg0 + h * R.qtiles + it.qtile];
+    const size_t prow = (size_t)(sg.part_base + it.split) * ABQ + (qi - q0);
     const float inv = l_r[r] > 0.f ? 1.f / l_r[r] : 0.f;
-    float* dst = a.part_o + prow * d + h * D;
+    float* dst = a.part_o + prow * D;
 #pragma unroll
     for (int i = 0; i < NDT; ++i) {
       const uint32_t col = i * 8 + tq * 2;
       if (col < D) dst[col] = o[i][r * 2] * inv;
       if (col + 1 < D) dst[col + 1] = o[i][r * 2 + 1] * inv;
     }
-    if (tq == 0) a.part_lse[prow * a.g.H + h] = l_r[r] > 0.f ? m_r[r] + log2f(l_r[r]) : -INFINITY;
+    if (tq == 0) a.part_lse[prow] = l_r[r] > 0.f ? m_r[r] + log2f(l_r[r]) : -INFINITY;
   }
 }
 
@@ -452,99 +453,127 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------- gate/norm ---
-// One warp per fresh row: merge split-K partials, silu(o) * u, layer norm.
-constexpr int GATE_WARPS = 8, GATE_MAXW = 256;  // per-warp cache of split weights
+// One warp per fresh row: merge the row's partial slots per head (log-sum-exp
+// weights, base 2), silu(o) * u, layer norm. When d % 32 == 0 and the head
+// width is a multiple of d/32, each lane owns d/32 contiguous columns of one
+// head (vector loads of every slot); otherwise lanes stride the columns.
+constexpr int GATE_WARPS = 8, GATE_MAXE = 16;  // d <= 512
 
+__device__ __forceinline__ float gate_merge_col(const GateArgs& a, const AttnSeg& sg, uint32_t ri, uint32_t c) {
+  float mx = -INFINITY;
+  for (uint32_t k = 0; k < sg.n_parts; ++k) mx = fmaxf(mx, a.part_lse[(size_t)(sg.part_base + k) * a.bm + ri]);
+  float num = 0.f, den = 0.f;
+  for (uint32_t k = 0; k < sg.n_parts; ++k) {
+    const size_t prow = (size_t)(sg.part_base + k) * a.bm + ri;
+    const float l = a.part_lse[prow];
+    if (l == -INFINITY) continue;
+    const float w = exp2f(l - mx);
+    num += w * a.part_o[prow * a.D + c];
+    den += w;
+  }
+  return den > 0.f ? num / den : 0.f;
+}
+
+template <int E>  // contiguous columns per lane
 __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) {
-  __shared__ float wsm[GATE_WARPS][GATE_MAXW];
   const int wid = threadIdx.x / 32;
   const int row = blockIdx.x * GATE_WARPS + wid;
   const int lane = threadIdx.x & 31;
   if (row >= (int)a.rows) return;
   const ReqDev R = a.reqs[a.row_req[row]];
-  const uint32_t i = row - R.q_row0, d = a.H * a.D;
-  const uint32_t nw = R.n_splits * a.H;
-  const bool cached = nw <= GATE_MAXW;
-  float* w = wsm[wid];
-  if (cached) {
-    // normalised merge weights w[s*H+h] = 2^(lse_s,h - max_s) / sum_s(...)
-    for (uint32_t p = lane; p < nw; p += 32) {
-      const uint32_t sp = p / a.H, h = p % a.H;
-      w[p] = a.part_lse[((size_t)R.part_base + (size_t)sp * R.n_q + i) * a.H + h];
-    }
-    __syncwarp();
-    for (uint32_t h = lane; h < a.H; h += 32) {
-      float mx = -INFINITY;
-      for (uint32_t sp = 0; sp < R.n_splits; ++sp) mx = fmaxf(mx, w[sp * a.H + h]);
-      float den = 0.f;
-      for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
-        const float l = w[sp * a.H + h];
-        const float e = l == -INFINITY ? 0.f : exp2f(l - mx);
-        w[sp * a.H + h] = e;
-        den += e;
-      }
-      const float inv = den > 0.f ? 1.f / den : 0.f;
-      for (uint32_t sp = 0; sp < R.n_splits; ++sp) w[sp * a.H + h] *= inv;
-    }
-    __syncwarp();
-  }
-  constexpr int MAXE = 16;  // d <= 512
-  float x[MAXE];
+  const uint32_t i = row - R.q_row0, qt = i / a.bm, ri = i % a.bm, d = a.H * a.D;
+  constexpr int NE = E > 0 ? E : GATE_MAXE;
+  float x[NE];
   float sum = 0.f;
+  if constexpr (E > 0) {
+    const uint32_t j0 = lane * E, h = j0 / a.D, c0 = j0 % a.D;
+    const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
+    float mx = -INFINITY;
+    for (uint32_t k = 0; k < sg.n_parts; ++k) mx = fmaxf(mx, a.part_lse[(size_t)(sg.part_base + k) * a.bm + ri]);
+    float acc[E];
 #pragma unroll
-  for (int e = 0; e < MAXE; ++e) {
-    const uint32_t j = lane + 32 * e;
-    x[e] = 0.f;
-    if (j >= d) continue;
-    const uint32_t h = j / a.D;
-    float o = 0.f;
-    if (cached) {
-      for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
-        const float ws = w[sp * a.H + h];
-        if (ws != 0.f) o += ws * a.part_o[((size_t)R.part_base + (size_t)sp * R.n_q + i) * d + j];
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
+    float den = 0.f;
+    for (uint32_t k = 0; k < sg.n_parts; ++k) {
+      const size_t prow = (size_t)(sg.part_base + k) * a.bm + ri;
+      const float l = a.part_lse[prow];
+      if (l == -INFINITY) continue;
+      const float w = exp2f(l - mx);
+      den += w;
+      const float* src = a.part_o + prow * a.D + c0;
+      if constexpr (E % 4 == 0) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(src + e);
+          acc[e] += w * v.x; acc[e + 1] += w * v.y; acc[e + 2] += w * v.z; acc[e + 3] += w * v.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] += w * src[e];
       }
-    } else {
-      float mx = -INFINITY;
-      for (uint32_t sp = 0; sp < R.n_splits; ++sp)
-        mx = fmaxf(mx, a.part_lse[((size_t)R.part_base + sp * R.n_q + i) * a.H + h]);
-      float num = 0.f, den = 0.f;
-      for (uint32_t sp = 0; sp < R.n_splits; ++sp) {
-        const size_t prow = (size_t)R.part_base + sp * R.n_q + i;
-        const float l = a.part_lse[prow * a.H + h];
-        if (l == -INFINITY) continue;
-        const float ws = exp2f(l - mx);
-        num += ws * a.part_o[prow * d + j];
-        den += ws;
-      }
-      o = den > 0.f ? num / den : 0.f;
     }
-    const float u = __bfloat162float(a.u[(size_t)row * d + j]);
-    x[e] = (o / (1.0f + expf(-o))) * u;
-    sum += x[e];
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    const __nv_bfloat16* up = a.u + (size_t)row * d + j0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float o = acc[e] * inv;
+      x[e] = (o / (1.0f + expf(-o))) * __bfloat162float(up[e]);
+      sum += x[e];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const uint32_t j = lane + 32 * e;
+      x[e] = 0.f;
+      if (j >= d) continue;
+      const uint32_t h = j / a.D;
+      const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
+      const float o = gate_merge_col(a, sg, ri, j % a.D);
+      x[e] = (o / (1.0f + expf(-o))) * __bfloat162float(a.u[(size_t)row * d + j]);
+      sum += x[e];
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffff, sum, off);
   const float mean = sum / (float)d;
   float var = 0.f;
 #pragma unroll
-  for (int e = 0; e < MAXE; ++e) {
-    const uint32_t j = lane + 32 * e;
+  for (int e = 0; e < NE; ++e) {
+    const uint32_t j = E > 0 ? lane * E + e : lane + 32 * e;
     if (j < d) { const float c = x[e] - mean; var += c * c; }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) var += __shfl_xor_sync(0xffffffff, var, off);
   var /= (float)d;
   const float inv = 1.0f / sqrtf(var + 1e-6f);
+  if constexpr (E > 0) {
+    __nv_bfloat16* op = a.out + (size_t)row * d + lane * E;
 #pragma unroll
-  for (int e = 0; e < MAXE; ++e) {
-    const uint32_t j = lane + 32 * e;
-    if (j < d) a.out[(size_t)row * d + j] = __float2bfloat16((x[e] - mean) * inv * a.ln_scale[j]);
+    for (int e = 0; e < E; ++e) op[e] = __float2bfloat16((x[e] - mean) * inv * a.ln_scale[lane * E + e]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const uint32_t j = lane + 32 * e;
+      if (j < d) a.out[(size_t)row * d + j] = __float2bfloat16((x[e] - mean) * inv * a.ln_scale[j]);
+    }
   }
 }
 
 void launch_gate_norm(const GateArgs& a, cudaStream_t s) {
   if (a.rows == 0) return;
-  gate_norm_kernel<<<(a.rows + GATE_WARPS - 1) / GATE_WARPS, GATE_WARPS * 32, 0, s>>>(a);
+  const uint32_t d = a.H * a.D, E = d % 32 == 0 ? d / 32 : 0;
+  const dim3 grid((a.rows + GATE_WARPS - 1) / GATE_WARPS), block(GATE_WARPS * 32);
+  if (E && a.D % E == 0) {
+    switch (E) {
+      case 1: gate_norm_kernel<1><<<grid, block, 0, s>>>(a); return;
+      case 2: gate_norm_kernel<2><<<grid, block, 0, s>>>(a); return;
+      case 4: gate_norm_kernel<4><<<grid, block, 0, s>>>(a); return;
+      case 8: gate_norm_kernel<8><<<grid, block, 0, s>>>(a); return;
+      case 16: gate_norm_kernel<16><<<grid, block, 0, s>>>(a); return;
+      default: break;
+    }
+  }
+  gate_norm_kernel<0><<<grid, block, 0, s>>>(a);
 }
 
 // -------------------------------------------------------- scatter/gather ---

@@ -31,13 +31,28 @@ struct ReqDev {
   uint64_t start;       // position of the first fresh row (= cached prefix length)
   uint32_t pages_off, n_pages;      // user pages (positions 0 .. start+n_hist-1)
   uint32_t scratch_off, n_scratch;  // candidate pages
-  uint32_t part_base;   // first partial row of this request (split-K attention)
-  uint32_t n_splits;
-  uint32_t split_keys;
+  uint32_t seg0;        // first attention segment of this request (head-major, then query tile)
+  uint32_t qtiles;      // query tiles of `bm` rows per head
+  uint32_t split_keys;  // mma.sync path: keys per split
   uint32_t user;
 };
 
-struct AttnItem {  // one CTA of the attention kernel
+// Attention work decomposition. A segment = (request, head, query tile of bm
+// rows) is one softmax problem; its partial results live in slots
+// part_base .. part_base + n_parts - 1, each slot = bm rows x D floats (O / l)
+// plus bm floats (log-sum-exp, base 2; -inf = empty). The split-K combine in
+// gate_norm_kernel merges a segment's slots.
+struct AttnSeg {
+  uint32_t req, head, qtile;
+  uint32_t n_tiles;     // tcgen05 path: 64-key tiles visible to the query tile
+  uint32_t part_base, n_parts;
+};
+// tcgen05 path: a piece = key tiles [lo, hi) of one segment, run by one CTA of
+// the persistent kernel; slot `part` (pipeline 0) and `part + 1` (pipeline 1).
+struct AttnPiece {
+  uint32_t seg, lo, hi, part;
+};
+struct AttnItem {  // mma.sync path: one CTA = (request, head, query tile, key split)
   uint32_t req, head, qtile, split;
 };
 
@@ -75,10 +90,13 @@ struct AttnArgs {
   const __nv_bfloat16* pool;
   const uint32_t* pages;
   const ReqDev* reqs;
-  const AttnItem* items;
-  uint32_t n_items;
-  float* part_o;            // [part_rows x d]
-  float* part_lse;          // [part_rows x H]
+  const AttnSeg* segs;
+  const AttnItem* items;    // mma.sync path: one per CTA
+  uint32_t n_items;         // mma.sync path: CTAs; tcgen05 path: persistent CTAs
+  const AttnPiece* pieces;  // tcgen05 path: pieces of CTA c = [cta_off[c], cta_off[c+1])
+  const uint32_t* cta_off;
+  float* part_o;            // [slots x bm x D]
+  float* part_lse;          // [slots x bm]
   PoolGeom g;
   uint32_t layer;
   float scale_log2;         // log2(e) / sqrt(D)
@@ -91,6 +109,8 @@ void launch_attention(const AttnArgs& a, cudaStream_t s);
 struct GateArgs {  // split combine + silu(o) * u + layer norm -> bf16
   const float* part_o;
   const float* part_lse;
+  const AttnSeg* segs;
+  uint32_t bm;              // query rows per segment (slot row stride)
   const __nv_bfloat16* u;
   const float* ln_scale;
   const uint32_t* row_req;
@@ -127,5 +147,25 @@ __host__ __device__ inline uint16_t tag_word(uint32_t user, uint64_t pos, uint32
 namespace mtkv_b200 {
 bool attn_tc_supported(const PoolGeom& g);
 int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g);
-void launch_attention_tc(const CUtensorMap& map, const AttnArgs& a, cudaStream_t s);
+int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g);
+void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s);
+int num_sms();
+}  // namespace mtkv_b200
+
+// ---- host-side attention planning (attn_plan.cpp) ----
+#include <vector>
+namespace mtkv_b200 {
+struct AttnPlan {
+  uint32_t bm = 128;               // query rows per segment
+  std::vector<AttnSeg> segs;
+  std::vector<AttnPiece> pieces;   // tcgen05 path
+  std::vector<uint32_t> cta_off;   // tcgen05 path, n_ctas + 1 entries
+  std::vector<AttnItem> items;     // mma.sync path
+  uint32_t n_slots = 0;
+  uint32_t n_ctas() const { return cta_off.empty() ? 0 : uint32_t(cta_off.size() - 1); }
+};
+constexpr uint32_t kTcBM = 128, kTcBN = 64;
+// Fills reqs[r].seg0/qtiles (and split_keys for the mma path) and the plan.
+// tcgen05: balanced contiguous key-tile ranges over `ctas` persistent CTAs.
+void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& plan);
 }  // namespace mtkv_b200

@@ -58,17 +58,24 @@ static int chunk_op(bool to_pool, void* pool, void* staging, const uint32_t* d_p
   return finish(e);
 }
 
-// out = merge of the two pipeline partials (log-sum-exp weights, base 2)
-__global__ void merge2_kernel(float* out, const float* part, const float* lse, uint32_t n_q, uint32_t H,
-                              uint32_t D) {
+// out[i][h*D + c] = log-sum-exp merge (base 2) of segment (h, i / bm)'s partial slots
+__global__ void merge_segs_kernel(float* out, const float* part, const float* lse, const AttnSeg* segs, uint32_t n_q,
+                                  uint32_t H, uint32_t D, uint32_t bm, uint32_t qtiles) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x, d = H * D;
   if (idx >= n_q * d) return;
-  const uint32_t i = idx / d, j = idx % d, h = j / D;
-  const float l0 = lse[size_t(i) * H + h], l1 = lse[(size_t(n_q) + i) * H + h];
-  const float m = fmaxf(l0, l1);
-  const float w0 = l0 == -INFINITY ? 0.f : exp2f(l0 - m), w1 = l1 == -INFINITY ? 0.f : exp2f(l1 - m);
-  const float den = w0 + w1;
-  out[idx] = den > 0.f ? (w0 * part[idx] + w1 * part[size_t(n_q) * d + idx]) / den : 0.f;
+  const uint32_t i = idx / d, j = idx % d, h = j / D, c = j % D, ri = i % bm;
+  const AttnSeg sg = segs[h * qtiles + i / bm];
+  float m = -INFINITY;
+  for (uint32_t k = 0; k < sg.n_parts; ++k) m = fmaxf(m, lse[size_t(sg.part_base + k) * bm + ri]);
+  float num = 0.f, den = 0.f;
+  for (uint32_t k = 0; k < sg.n_parts; ++k) {
+    const size_t prow = size_t(sg.part_base + k) * bm + ri;
+    if (lse[prow] == -INFINITY) continue;
+    const float w = exp2f(lse[prow] - m);
+    num += w * part[prow * D + c];
+    den += w;
+  }
+  out[idx] = den > 0.f ? num / den : 0.f;
 }
 
 extern "C" {
@@ -101,56 +108,63 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   r.start = p_pre;
   r.pages_off = 0;
   r.n_pages = uint32_t((n_keys + g.S - 1) / g.S);
-  r.part_base = 0;
-  r.split_keys = 0xFFFFFF00u;
   const char* force = std::getenv("MTKV_ATTN");
   const bool tc = attn_tc_supported(g) && !(force && std::string(force) == "mma");
-  r.n_splits = tc ? 2 : 1;  // the tcgen05 kernel emits one partial per softmax pipeline
-  const uint32_t bq = (tc || n_q > 64) ? 128 : 64;
-  const uint32_t qtiles = (n_q + bq - 1) / bq, n_items = g.H * qtiles;
-  AttnItem* hi = new AttnItem[n_items];
-  uint32_t k = 0;
-  for (uint32_t h = 0; h < g.H; ++h)
-    for (uint32_t t = 0; t < qtiles; ++t) hi[k++] = AttnItem{0, h, t, 0};
+  AttnPlan plan;
+  plan_attention(&r, 1, g, tc, tc ? uint32_t(num_sms()) : 0, plan);
+  const uint32_t n_items = tc ? plan.n_ctas() : uint32_t(plan.items.size());
+  // one device allocation: request | segments | items or pieces + CTA offsets | lse | partials
+  size_t off = 0;
+  auto carve = [&](size_t bytes) { const size_t o = off; off = (off + bytes + 255) & ~size_t(255); return o; };
+  const size_t o_req = carve(sizeof(ReqDev));
+  const size_t o_seg = carve(plan.segs.size() * sizeof(AttnSeg));
+  const size_t o_items = carve(plan.items.size() * sizeof(AttnItem));
+  const size_t o_pieces = carve(plan.pieces.size() * sizeof(AttnPiece));
+  const size_t o_cta = carve(plan.cta_off.size() * sizeof(uint32_t));
+  const size_t o_lse = carve(size_t(plan.n_slots) * plan.bm * sizeof(float));
+  const size_t o_part = carve(size_t(plan.n_slots) * plan.bm * g.D * sizeof(float));
   char* buf = nullptr;
-  const size_t part_bytes = tc ? size_t(2) * n_q * g.d * sizeof(float) : 0;
-  const size_t bytes = 256 + n_items * sizeof(AttnItem) + size_t(2) * n_q * g.H * sizeof(float) + part_bytes;
-  cudaError_t e = cudaMallocAsync((void**)&buf, bytes, s);
-  if (e != cudaSuccess) { delete[] hi; return finish(e); }
-  ReqDev* dr = reinterpret_cast<ReqDev*>(buf);
-  AttnItem* di = reinterpret_cast<AttnItem*>(buf + 256);
-  float* lse = reinterpret_cast<float*>(buf + 256 + n_items * sizeof(AttnItem));
-  float* part = tc ? lse + size_t(2) * n_q * g.H : nullptr;
-  e = cudaMemcpyAsync(dr, &r, sizeof(r), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(di, hi, n_items * sizeof(AttnItem), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  delete[] hi;
+  cudaError_t e = cudaMallocAsync((void**)&buf, off, s);
+  if (e != cudaSuccess) return finish(e);
+  auto up = [&](size_t o, const void* src, size_t bytes) {
+    if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(buf + o, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  up(o_req, &r, sizeof(r));
+  up(o_seg, plan.segs.data(), plan.segs.size() * sizeof(AttnSeg));
+  up(o_items, plan.items.data(), plan.items.size() * sizeof(AttnItem));
+  up(o_pieces, plan.pieces.data(), plan.pieces.size() * sizeof(AttnPiece));
+  up(o_cta, plan.cta_off.data(), plan.cta_off.size() * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host plan vectors die with this scope
   AttnArgs a{};
   a.q = static_cast<const __nv_bfloat16*>(q);
   a.pool = static_cast<const __nv_bfloat16*>(pool);
   a.pages = d_pages;
-  a.reqs = dr;
-  a.items = di;
+  a.reqs = reinterpret_cast<const ReqDev*>(buf + o_req);
+  a.segs = reinterpret_cast<const AttnSeg*>(buf + o_seg);
+  a.items = reinterpret_cast<const AttnItem*>(buf + o_items);
+  a.pieces = reinterpret_cast<const AttnPiece*>(buf + o_pieces);
+  a.cta_off = reinterpret_cast<const uint32_t*>(buf + o_cta);
   a.n_items = n_items;
-  a.part_o = tc ? part : out;
-  a.part_lse = lse;
+  a.part_o = reinterpret_cast<float*>(buf + o_part);
+  a.part_lse = reinterpret_cast<float*>(buf + o_lse);
   a.g = g;
   a.layer = layer;
-  a.bq = bq;
+  a.bq = plan.bm;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
   if (e == cudaSuccess) {
     if (tc) {
-      alignas(64) CUtensorMap map;
-      if (make_pool_map(&map, pool, g)) {
+      alignas(64) CUtensorMap pmap, qmap;
+      if (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, n_q, g)) {
         cudaFreeAsync(buf, s);
         set_last_error("paged_attention: cuTensorMapEncodeTiled failed");
         return MTKV_ERROR;
       }
-      launch_attention_tc(map, a, s);
-      merge2_kernel<<<(n_q * g.d + 255) / 256, 256, 0, s>>>(out, part, lse, n_q, g.H, g.D);
+      launch_attention_tc(pmap, qmap, a, s);
     } else {
       launch_attention(a, s);
     }
+    merge_segs_kernel<<<(n_q * g.d + 255) / 256, 256, 0, s>>>(out, a.part_o, a.part_lse, a.segs, n_q, g.H, g.D,
+                                                               plan.bm, r.qtiles);
   }
   cudaFreeAsync(buf, s);
   return finish(e);

@@ -135,6 +135,31 @@ def test_value_engine_rankings():
     assert total > 0 and agree == total
 
 
+def test_pipelined_rankings_match_synchronous():
+    """submit()/rankings(ticket) with up to 3 batches in flight returns exactly the
+    rankings of the synchronous process_batch()/last_rankings() path; tickets older
+    than the 4-batch result ring are refused."""
+    case = [c for c in golden_cases("value") if c["name"] == "value10"][0]
+    m = mtkv.ModelConfig(**case["model"])
+    bs = batches(case["trace"], 2)
+    mk = lambda: mtkv.Engine(_kv(case["kv"]), mode="hierarchical", backend="value", batch_size=2, model=m)
+    sync = mk()
+    want = []
+    for b in bs:
+        sync.process_batch(b)
+        want.append(sync.last_rankings())
+    pipe = mk()
+    got, pending = [], []
+    for b in bs:
+        pending.append(pipe.submit(b))
+        if len(pending) > 3:
+            got.append(pipe.rankings(pending.pop(0)))
+    got += [pipe.rankings(t) for t in pending]
+    assert got == want
+    with pytest.raises(mtkv.Error):
+        pipe.rankings(mtkv.Ticket(0, [1, 1]))
+
+
 def test_model_dims_of_bench_config():
     """d = 256 (H=2, D=128): vector/tensor-core paths at the bench width vs the oracle."""
     kv = dict(num_layers=2, num_heads=2, head_dim=128, page_size=32, chunk_size=64, device_pages=64,
@@ -168,7 +193,12 @@ def _paged_pool(L, P, S, d, seed=0):
 
 
 @pytest.mark.parametrize("H,D,S,p_pre,n_q", [(2, 128, 32, 1000, 72), (4, 64, 16, 0, 130), (1, 32, 8, 333, 5),
-                                               (2, 16, 32, 4096, 64), (1, 8, 4, 17, 3)])
+                                               (2, 16, 32, 4096, 64), (1, 8, 4, 17, 3),
+                                               # persistent tcgen05 kernel: many pieces per segment,
+                                               # several query tiles, 1-tile pieces, single rows
+                                               (2, 128, 64, 20000, 72), (4, 128, 32, 5000, 300),
+                                               (1, 64, 8, 3000, 1), (3, 128, 16, 777, 129),
+                                               (2, 64, 64, 0, 1000)])
 def test_paged_attention_op_vs_torch_fp32(H, D, S, p_pre, n_q):
     d, L = H * D, 2
     n_keys = p_pre + n_q
