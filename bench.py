@@ -198,8 +198,10 @@ def run_b200(args, cfg):
     tok_bytes = kv.token_kv_bytes()
     host_mb = int(1.3 * (cfg["users"] * (cfg["history"] + 2 * kv.chunk_size) + len(revisits) * cfg["delta"])
                   * tok_bytes / 2**20) + 1024
+    ppu = -(-(cfg["history"] + 16 * cfg["delta"]) // cfg["page"])
     eng = mtkv.Engine(kv, cost, mode="hierarchical", backend="value", batch_size=B, model=model,
-                      device=local, host_reserve_mb=host_mb)
+                      device=local, host_reserve_mb=host_mb, planner=args.planner,
+                      max_users=cfg["users"] + 64, max_user_pages=2 * ppu + 64)
     # ---- warm-up: prefill histories (untimed), then the first revisit batches ----
     pb = max(1, 65536 // cfg["history"])
     for i in range(0, len(prefill), pb):
@@ -237,6 +239,8 @@ def run_b200(args, cfg):
     # ---- phase B: per-batch device latency (p50/p99) + per-launch attention timing ----
     eng.set_profile(True)
     eng_lat, attn_ms, attn_launches, attn_bytes = [], 0.0, 0, 0
+    copy_stat = [0.0, 0, 0.0, 0, 0, 0]  # scatter ms, chunks, gather ms, chunks, launches, launches
+    plan_ms, ctl_ms = [], []
     d = cfg["H"] * cfg["D"]
     rb0 = eng.report()
     k0 = warm + K
@@ -247,6 +251,12 @@ def run_b200(args, cfg):
         ms, n = eng.last_attention_ms()
         attn_ms += ms
         attn_launches += n
+        pm, km = eng.last_plan_ms()
+        plan_ms.append(pm)
+        ctl_ms.append(km)
+        sm, sc, gm, gc = eng.last_chunk_copy_ms()
+        copy_stat[0] += sm; copy_stat[1] += sc; copy_stat[2] += gm; copy_stat[3] += gc
+        copy_stat[4] += 1 if sc else 0; copy_stat[5] += 1 if gc else 0
         for p in eng.plans():
             keys = p["history_len"] + p["delta"] + p["num_candidates"]
             rows = p["fresh_history"] + p["delta"] + p["num_candidates"]
@@ -332,7 +342,22 @@ def run_b200(args, cfg):
                      "avg_launch_us": avg_launch_s * 1e6,
                      "bytes_per_launch": attn_bytes / max(attn_launches, 1)},
         "clocks": clk,
+        "control_plane": {"planner": args.planner,
+                          "plan_ms_per_batch": float(np.mean(plan_ms)) if plan_ms else None,
+                          "device_planner_kernel_us": float(np.mean(ctl_ms)) * 1e3 if args.planner == "device" else None,
+                          "note": "host wall time of prepare_metadata + schedule + bookkeeping per batch (phase B)"},
     }
+    # KV movement kernels (north-star "KV-gather at >= 60% of HBM roofline"): algorithmic
+    # bytes = read + write of every moved chunk ([L][2][chunk][d] bf16)
+    cb = kv.chunk_bytes()
+    kern = {}
+    for name, ms, ch, nl in (("chunk_scatter (onload: staging -> pages)", copy_stat[0], copy_stat[1], copy_stat[4]),
+                             ("chunk_gather (offload: pages -> slots)", copy_stat[2], copy_stat[3], copy_stat[5])):
+        if ch:
+            gbs = 2 * ch * cb / (ms / 1e3) / 1e9
+            kern[name] = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                          "launches": nl, "avg_launch_us": ms / nl * 1e3, "bytes_per_launch": 2 * ch * cb / nl}
+    line["roofline"]["other_kernels"] = kern
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -385,6 +410,8 @@ def main():
     ap.add_argument("--users", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--planner", default="host", choices=["host", "device"],
+                    help="control plane: host C++ planner or the GPU (devctl.cu) lookup/LRU/victim kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -113,6 +113,9 @@ typedef struct {
   uint32_t keep_logits;      /* 1: keep full [n x vocab] logits of the last batch */
   uint32_t profile;          /* 1: time every attention launch with CUDA events */
   uint64_t host_reserve_mb;  /* pinned host store allocated up front (0: grow on demand) */
+  uint32_t device_planner;   /* 1: user lookup, LRU update, victim selection and page allocation
+                                (manager.cpp:74 prepare_metadata) run on the GPU over device tables */
+  uint32_t max_users;        /* device planner: user-table capacity (0 = 65536) */
 } mtkv_engine_options;
 
 /* ---- configuration (core.cpp) ---- */
@@ -161,6 +164,10 @@ int mtkv_engine_last_rankings(mtkv_engine* e, uint32_t* out, uint64_t cap);
  * host can enqueue batch i+1's onload before reading batch i. */
 int mtkv_engine_batch_rankings(mtkv_engine* e, uint64_t ticket, uint32_t* out, uint64_t cap);
 uint64_t mtkv_engine_batches_submitted(const mtkv_engine* e);
+/* control-plane cost of the last batch: host wall ms of planning (prepare_metadata,
+ * schedule, bookkeeping; includes the device planner's round trip when enabled)
+ * and the device planner kernel's ms (0 with the host planner) */
+void mtkv_engine_last_plan_ms(const mtkv_engine* e, double* plan_ms, double* ctl_kernel_ms);
 /* check_conservation (sim.cpp:60), tag backend: reads back the whole device
  * pool and host store and verifies every resident token's identity */
 int mtkv_engine_check_conservation(mtkv_engine* e);
@@ -172,6 +179,11 @@ int64_t mtkv_engine_read_user_kv(mtkv_engine* e, uint32_t user, uint32_t layer,
 double mtkv_engine_last_batch_ms(mtkv_engine* e);
 /* device time of the attention kernels of the last batch (ms) and their launch count */
 double mtkv_engine_last_attention_ms(mtkv_engine* e, uint32_t* launches);
+/* profile mode: device ms of the last batch's onload scatter (staging -> pages,
+ * store.hpp:89) and offload gather (pages -> offload slots, store.hpp:106), with
+ * the chunk counts they moved */
+int mtkv_engine_last_chunk_copy_ms(mtkv_engine* e, double* scatter_ms, uint32_t* scatter_chunks,
+                                   double* gather_ms, uint32_t* gather_chunks);
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e);
 /* toggles per-launch CUDA-event timing of the attention kernels */
 void mtkv_engine_set_profile(mtkv_engine* e, uint32_t on);

@@ -106,7 +106,8 @@ class _EngineOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("backend", C.c_int), ("batch_size", C.c_uint32),
                 ("seed", C.c_uint64), ("model", _ModelCfg), ("device", C.c_int),
                 ("max_batch_tokens", C.c_uint32), ("max_user_pages", C.c_uint32),
-                ("keep_logits", C.c_uint32), ("profile", C.c_uint32), ("host_reserve_mb", C.c_uint64)]
+                ("keep_logits", C.c_uint32), ("profile", C.c_uint32), ("host_reserve_mb", C.c_uint64),
+                ("device_planner", C.c_uint32), ("max_users", C.c_uint32)]
 
 
 class _GenCfg(C.Structure):
@@ -125,8 +126,10 @@ EXPORTED_SYMBOLS = [
     "mtkv_engine_create", "mtkv_engine_destroy", "mtkv_engine_process_batch", "mtkv_engine_run",
     "mtkv_engine_drain", "mtkv_engine_synchronize", "mtkv_engine_last_logits",
     "mtkv_engine_last_rankings", "mtkv_engine_batch_rankings", "mtkv_engine_batches_submitted",
+    "mtkv_engine_last_plan_ms",
     "mtkv_engine_check_conservation", "mtkv_engine_read_user_kv",
-    "mtkv_engine_last_batch_ms", "mtkv_engine_last_attention_ms", "mtkv_engine_kernel_launches",
+    "mtkv_engine_last_batch_ms", "mtkv_engine_last_attention_ms", "mtkv_engine_last_chunk_copy_ms",
+    "mtkv_engine_kernel_launches",
     "mtkv_engine_set_profile",
     "mtkv_report", "mtkv_last_plans", "mtkv_last_evictions", "mtkv_known_users", "mtkv_user_state",
     "mtkv_user_pages", "mtkv_lru_snapshot", "mtkv_evict_user", "mtkv_is_locked",
@@ -171,11 +174,13 @@ def lib():
         "mtkv_engine_last_rankings": (C.c_int, [vp, u32p, u64]),
         "mtkv_engine_batch_rankings": (C.c_int, [vp, u64, u32p, u64]),
         "mtkv_engine_batches_submitted": (u64, [vp]),
+        "mtkv_engine_last_plan_ms": (None, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "mtkv_engine_check_conservation": (C.c_int, [vp]),
         "mtkv_engine_read_user_kv": (C.c_int64, [vp, u32, u32, C.POINTER(C.c_uint16),
                                                  C.POINTER(C.c_uint16), u64]),
         "mtkv_engine_last_batch_ms": (C.c_double, [vp]),
         "mtkv_engine_last_attention_ms": (C.c_double, [vp, u32p]),
+        "mtkv_engine_last_chunk_copy_ms": (C.c_int, [vp, C.POINTER(C.c_double), u32p, C.POINTER(C.c_double), u32p]),
         "mtkv_engine_kernel_launches": (u64, [vp]),
         "mtkv_engine_set_profile": (None, [vp, u32]),
         "mtkv_report": (C.c_int, [vp, C.c_int, C.POINTER(_Report)]),
@@ -243,6 +248,10 @@ class KVConfig:
 
     def token_kv_bytes(self) -> int:
         return self.num_layers * 2 * self.num_heads * self.head_dim * self.bytes_per_element
+
+    def chunk_bytes(self) -> int:
+        """bytes of one host chunk / staging slot: [L][2][chunk_size][H*D]"""
+        return self.chunk_size * self.token_kv_bytes()
 
     def validate(self) -> None:
         _check(lib().mtkv_kv_config_validate(C.byref(self._c())))
@@ -474,7 +483,8 @@ class Engine(_ManagerView):
     def __init__(self, kv: KVConfig, cost: CostModel | None = None, mode: str = "hierarchical",
                  backend: str = "tag", batch_size: int = 1, model: ModelConfig | None = None,
                  device: int = 0, keep_logits: bool = False, profile: bool = False, seed: int = 1,
-                 host_reserve_mb: int = 0):
+                 host_reserve_mb: int = 0, planner: str = "host", max_users: int = 0,
+                 max_user_pages: int = 0):
         self.kv, self.mode, self.backend, self.batch_size = kv, mode, backend, batch_size
         self.model = model
         if backend == "value" and model is None:
@@ -485,6 +495,10 @@ class Engine(_ManagerView):
             o.model = _ModelCfg(model.num_layers, model.num_heads, model.head_dim, model.vocab, model.seed)
         o.device, o.keep_logits, o.profile = device, int(keep_logits), int(profile)
         o.host_reserve_mb = int(host_reserve_mb)
+        if planner not in ("host", "device"):
+            raise Error("planner must be 'host' or 'device'")
+        o.device_planner = int(planner == "device")
+        o.max_users, o.max_user_pages = int(max_users), int(max_user_pages)
         self._h = lib().mtkv_engine_create(C.byref(kv._c()), C.byref((cost or CostModel())._c()),
                                            C.byref(o))
         if not self._h:
@@ -580,6 +594,19 @@ class Engine(_ManagerView):
         n = C.c_uint32(0)
         ms = lib().mtkv_engine_last_attention_ms(self._h, C.byref(n))
         return float(ms), int(n.value)
+
+    def last_plan_ms(self):
+        """(host planning wall ms, device planner kernel ms) of the last batch."""
+        a, b = C.c_double(), C.c_double()
+        lib().mtkv_engine_last_plan_ms(self._h, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def last_chunk_copy_ms(self):
+        """(scatter_ms, scatter_chunks, gather_ms, gather_chunks) of the last batch (profile mode)."""
+        sm, gm = C.c_double(), C.c_double()
+        sc, gc = C.c_uint32(), C.c_uint32()
+        _check(lib().mtkv_engine_last_chunk_copy_ms(self._h, C.byref(sm), C.byref(sc), C.byref(gm), C.byref(gc)))
+        return sm.value, sc.value, gm.value, gc.value
 
     def set_profile(self, on: bool) -> None:
         lib().mtkv_engine_set_profile(self._h, int(on))

@@ -50,12 +50,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes instead of re-polling (polling warps steal issue slots
+// from the softmax warps sharing their SM sub-partition)
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 __device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
@@ -73,6 +76,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
           s32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
       : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, %1;\n@px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -96,6 +107,9 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
+}
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc_) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc_) : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
@@ -121,6 +135,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
       "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -166,7 +187,9 @@ struct TcCfg {
   static constexpr int NK = D == 128 ? 5 : 8;            // K ring stages
   static constexpr int NV = D == 128 ? 5 : 8;            // V ring stages
   static constexpr uint32_t S_COL = 0, P_COL = BN, O_COL = BN + BN / 2, PIPE = BN + BN / 2 + D;
-  static constexpr uint32_t TMEM_COLS = 2 * PIPE <= 256 ? 256 : 512;
+  static constexpr uint32_t Q_COL = 2 * PIPE;            // Q (bf16x2) after the two pipelines
+  static constexpr uint32_t TMEM_COLS = Q_COL + D / 2 <= 256 ? 256 : 512;
+  static_assert(Q_COL + D / 2 <= 512, "TMEM budget");
   static constexpr size_t SMEM = 1024 + 2 * Q_BYTES + size_t(NK + NV) * T_BYTES + 256;
   static_assert(SMEM <= 232448, "shared memory budget");
 };
@@ -311,52 +334,74 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: non-blocking event loop over both pipelines ----------------
-    if (lane == 0 && pe > pb) {
+    // ---------------- MMA issuer: S(g+2) is issued before PV(g) ----------------
+    // Tiles alternate between the two softmax pipelines. The whole warp runs the (uniform) control flow so descriptor
+    // arithmetic stays on the uniform datapath; one elected lane issues.
+    if (pe > pb) {
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
           (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+      const uint64_t dq0 = sdesc(s32(sQ), 16, 1024), dk0 = sdesc(s32(sK), 16, 1024), dv0 = sdesc(s32(sV), KBLK, 1024);
+      const bool leader = elect_one();
       TileCursor cs, cv;
       cs.init(a, pb, pe);
       cv.init(a, pb, pe);
-      while (cv.pc < pe) {
-        bool progressed = false;
-        // PV first: it frees a V stage and unblocks the owning softmax pipeline
-        if (cv.g < cs.g) {
-          const uint32_t p = cv.j & 1, u = p ? cv.c1 : cv.c0, stv = cv.g % NV;
-          if (mbar_ready(&p_full[p], u & 1) && mbar_ready(&full_v[stv], (cv.g / NV) & 1)) {
-            tc_after();
-            const uint32_t v_addr = s32(sV + stv * T_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk)
-              mma_ts(tmem + p * C::PIPE + C::O_COL, tmem + p * C::PIPE + C::P_COL + kk * 8,
-                     sdesc(v_addr + kk * 2048, KBLK, 1024), idesc_o, (cv.j >= 2 || kk > 0) ? 1u : 0u);
-            mma_commit(&o_done[p]);
-            mma_commit(&empty_v[stv]);
-            ATTN_TR(2, cv.g);
-            cv.next(a);
-            progressed = true;
-          }
-        }
-        if (cs.pc < pe && cs.g < cv.g + 2) {  // at most one S ahead per pipeline
-          const uint32_t p = cs.j & 1, u = p ? cs.c1 : cs.c0, stk = cs.g % NK, qb = cs.k & 1;
-          if (mbar_ready(&full_k[stk], (cs.g / NK) & 1) && (u == 0 || mbar_ready(&s_free[p], (u - 1) & 1)) &&
-              (cs.j != 0 || mbar_ready(&q_full[qb], (cs.k >> 1) & 1))) {
-            tc_after();
-            const uint32_t q_addr = s32(sQ + qb * Q_BYTES), k_addr = s32(sK + stk * T_BYTES);
+      auto issue_s = [&]() {
+        const uint32_t p = cs.j & 1, u = p ? cs.c1 : cs.c0, stk = cs.g % NK, qb = cs.k & 1;
+        if (leader) ATTN_TR(9, cs.g);
+        if (cs.j == 0) {
+          // new piece: copy its Q (landed by TMA) into TMEM, in order with the
+          // previous piece's S MMAs that still read the old Q
+          mbar_wait(&q_full[qb], (cs.k >> 1) & 1);
+          tc_after();
+          if (leader) {
+            const uint64_t aq = dq0 + ((qb * Q_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
-              mma_f16(tmem + p * C::PIPE + C::S_COL, sdesc(q_addr + (kk / 4) * QBLK + (kk % 4) * 32, 16, 1024),
-                      sdesc(k_addr + (kk / 4) * KBLK + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
-            mma_commit(&s_full[p]);
-            mma_commit(&empty_k[stk]);
-            if (cs.t + 1 == cs.hi) mma_commit(&q_empty[qb]);  // last S of the piece: Q buffer reusable
-            ATTN_TR(1, cs.g);
-            cs.next(a);
-            progressed = true;
+              tmem_cp_128x256b(tmem + C::Q_COL + kk * 8, aq + (((kk / 4) * QBLK + (kk % 4) * 32) >> 4));
+            mma_commit(&q_empty[qb]);  // smem Q buffer reusable once copied
           }
         }
-        if (!progressed) __nanosleep(20);
+        if (u > 0) mbar_wait(&s_free[p], (u - 1) & 1);
+        mbar_wait(&full_k[stk], (cs.g / NK) & 1);
+        tc_after();
+        if (leader) {
+          const uint64_t bk = dk0 + ((stk * T_BYTES) >> 4);
+          const uint32_t d_tmem = tmem + p * C::PIPE + C::S_COL;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_ts(d_tmem, tmem + C::Q_COL + kk * 8, bk + (((kk / 4) * KBLK + (kk % 4) * 32) >> 4), idesc_s, kk > 0);
+          mma_commit(&s_full[p]);
+          mma_commit(&empty_k[stk]);
+          ATTN_TR(1, cs.g);
+        }
+        __syncwarp();
+        cs.next(a);
+      };
+      // S runs two tiles ahead of PV: S(g+2) only needs pipeline (g & 1) to have
+      // loaded S(g) into registers, so it executes while that pipeline is still
+      // computing P(g), and the pipeline finds its next S ready when it finishes.
+      issue_s();
+      if (cs.pc < pe) issue_s();
+      while (cv.pc < pe) {
+        if (cs.pc < pe) issue_s();
+        const uint32_t p = cv.j & 1, u = p ? cv.c1 : cv.c0, stv = cv.g % NV;
+        if (leader) ATTN_TR(10, cv.g);
+        mbar_wait(&p_full[p], u & 1);
+        mbar_wait(&full_v[stv], (cv.g / NV) & 1);
+        tc_after();
+        if (leader) {
+          const uint64_t bv = dv0 + ((stv * T_BYTES) >> 4);
+          const uint32_t d_tmem = tmem + p * C::PIPE + C::O_COL, a_tmem = tmem + p * C::PIPE + C::P_COL;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            mma_ts(d_tmem, a_tmem + kk * 8, bv + ((kk * 2048) >> 4), idesc_o, (cv.j >= 2 || kk > 0) ? 1u : 0u);
+          mma_commit(&o_done[p]);
+          mma_commit(&empty_v[stv]);
+          ATTN_TR(2, cv.g);
+        }
+        __syncwarp();
+        cv.next(a);
       }
     }
   } else if (warp >= 4) {
@@ -383,6 +428,11 @@ __global__ void __launch_bounds__(384, 1)
       // valid keys of this row: user keys [0, u_end), candidate keys [KAp, c_end)
       const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
       const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
+      // the same bounds relative to the piece's first key, clamped to [0, span] (32-bit per tile)
+      const uint64_t kb0 = uint64_t(P.lo) * BN;
+      const int64_t span = int64_t(P.hi - P.lo) * BN;
+      auto rel = [&](uint64_t x) { return int(min(max(int64_t(x) - int64_t(kb0), int64_t(0)), span)); };
+      const int ue = rel(u_end), cl = rel(KAp), ce = rel(c_end);
       float m_ref = -INFINITY, l_run = 0.f;
       uint32_t mine = 0;
       for (uint32_t t = P.lo + p; t < P.hi; t += 2, ++u, ++mine) {
@@ -393,47 +443,53 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_col + c * 32, s + c * 32);
         tmem_wait_ld();
+        if (threadIdx.x % 128 == 0) ATTN_TR(6, u * 2 + p);
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[p]);
-        const uint64_t kb = uint64_t(t) * BN;
-        const int cu = int(u_end > kb ? (u_end - kb < uint64_t(BN) ? u_end - kb : uint64_t(BN)) : 0);
-        const int c_lo = int(KAp > kb ? (KAp - kb < uint64_t(BN) ? KAp - kb : uint64_t(BN)) : 0);
-        const int c_hi = int(c_end > kb ? (c_end - kb < uint64_t(BN) ? c_end - kb : uint64_t(BN)) : 0);
-        float mx = -INFINITY;
-        if (cu == BN) {
-#pragma unroll
-          for (int c = 0; c < BN; ++c) {
-            s[c] *= a.scale_log2;
-            mx = fmaxf(mx, s[c]);
-          }
-        } else {
+        const int kb = int(t - P.lo) * BN;
+        const int cu = min(max(ue - kb, 0), BN), c_lo = min(max(cl - kb, 0), BN), c_hi = min(max(ce - kb, 0), BN);
+        if (cu != BN) {
 #pragma unroll
           for (int c = 0; c < BN; ++c) {
             const bool ok = c < cu || (c >= c_lo && c < c_hi);
-            s[c] = ok ? s[c] * a.scale_log2 : -INFINITY;
-            mx = fmaxf(mx, s[c]);
+            s[c] = ok ? s[c] : -INFINITY;
           }
         }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
+#pragma unroll
+        for (int c = 0; c < BN; ++c) m4[c & 3] = fmaxf(m4[c & 3], s[c]);
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * a.scale_log2;
         float alpha = 1.f;
-        if (mx > m_ref + kRescale) {
+        if (mx > m_ref + kRescale) {  // lazy rescale: p <= 2^8 between rescales
           alpha = m_ref == -INFINITY ? 0.f : ex2(m_ref - mx);
           m_ref = mx;
         }
-        const float mref = m_ref == -INFINITY ? 0.f : m_ref;
-        float rs = 0.f;
+        const float nmref = m_ref == -INFINITY ? 0.f : -m_ref;
+        float r4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
-          s[c] = ex2(s[c] - mref);
-          rs += s[c];
+          s[c] = ex2(fmaf(s[c], a.scale_log2, nmref));
+          r4[c & 3] += s[c];
         }
+        const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
         l_run = l_run * alpha + rs;
+        if (threadIdx.x % 128 == 0) ATTN_TR(7, u * 2 + p);
         if (u > 0) {  // this pipeline's previous PV must finish before P / O are touched
           mbar_wait(&o_done[p], (u - 1) & 1);
           tc_after();
         }
-        if (mine > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        if (threadIdx.x % 128 == 0) ATTN_TR(8, u * 2 + p);
+        // P -> TMEM in two halves (keeps the live register set small), then the lazy O rescale
 #pragma unroll
+        for (int hlf = 0; hlf < 2; ++hlf) {
+          uint32_t pk[BN / 4];
+#pragma unroll
+          for (int c = 0; c < BN / 4; ++c) pk[c] = pack2(s[hlf * (BN / 2) + 2 * c], s[hlf * (BN / 2) + 2 * c + 1]);
+          tmem_st16(p_col + hlf * (BN / 4), pk);
+        }
+        if (mine > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             float o[32];
             tmem_ld32(o_col + c * 32, o);
@@ -443,17 +499,15 @@ __global__ void __launch_bounds__(384, 1)
             tmem_st32(o_col + c * 32, o);
           }
         }
-        uint32_t pk[BN / 2];
-#pragma unroll
-        for (int c = 0; c < BN / 2; ++c) pk[c] = pack2(s[2 * c], s[2 * c + 1]);
-        tmem_st32(p_col, reinterpret_cast<const float*>(pk));
         tmem_wait_st();
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[p]);
         if (threadIdx.x % 128 == 0) ATTN_TR(4, u * 2 + p);
+        if (threadIdx.x % 128 == 96) ATTN_TR(11, u * 2 + p);
       }
       // epilogue: this pipeline's O / l and lse (base 2) into slot part + p
+      if (threadIdx.x == 128) ATTN_TR(5, 3 + 2 * (pc - pb));
       const uint32_t qi = q0 + r;
       if (mine > 0) {
         mbar_wait(&o_done[p], (u - 1) & 1);
@@ -476,6 +530,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
       if (qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
+      if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
       tc_before();
     }
     if (threadIdx.x == 128) ATTN_TR(5, 2);

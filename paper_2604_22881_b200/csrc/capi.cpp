@@ -241,6 +241,10 @@ int mtkv_engine_batch_rankings(mtkv_engine* e, uint64_t ticket, uint32_t* out, u
 
 uint64_t mtkv_engine_batches_submitted(const mtkv_engine* e) { return e->e.batches_submitted(); }
 
+void mtkv_engine_last_plan_ms(const mtkv_engine* e, double* plan_ms, double* ctl_kernel_ms) {
+  e->e.last_plan_ms(plan_ms, ctl_kernel_ms);
+}
+
 int mtkv_engine_check_conservation(mtkv_engine* e) {
   std::string err;
   const int rc = e->e.check_conservation(err);
@@ -257,6 +261,10 @@ int64_t mtkv_engine_read_user_kv(mtkv_engine* e, uint32_t user, uint32_t layer, 
 
 double mtkv_engine_last_batch_ms(mtkv_engine* e) { return e->e.last_batch_ms(); }
 double mtkv_engine_last_attention_ms(mtkv_engine* e, uint32_t* launches) { return e->e.last_attention_ms(launches); }
+int mtkv_engine_last_chunk_copy_ms(mtkv_engine* e, double* scatter_ms, uint32_t* scatter_chunks, double* gather_ms,
+                                   uint32_t* gather_chunks) {
+  return e->e.last_chunk_copy_ms(scatter_ms, scatter_chunks, gather_ms, gather_chunks);
+}
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e) { return e->e.launches; }
 void mtkv_engine_set_profile(mtkv_engine* e, uint32_t on) { e->e.set_profile(on); }
 

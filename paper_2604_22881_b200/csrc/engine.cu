@@ -9,6 +9,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -95,6 +96,8 @@ Engine::~Engine() {
       cudaEventDestroy(ev_done_[k]); cudaEventDestroy(ev_start_[k]);
     }
     for (auto e : ev_attn_) cudaEventDestroy(e);
+    for (auto e : ev_copy_)
+      if (e) cudaEventDestroy(e);
     cudaStreamDestroy(comp_); cudaStreamDestroy(h2d_); cudaStreamDestroy(d2h_);
   }
 }
@@ -224,6 +227,22 @@ int Engine::init(std::string& err) {
     }
   }
   if (value_) init_weights();
+  if (opt_.device_planner) {
+    if (recompute_) {
+      err = "engine: the device planner needs a cached mode (gpu_only or hierarchical)";
+      return MTKV_ERROR;
+    }
+    const uint32_t max_users = opt_.max_users ? opt_.max_users : 65536;
+    const uint32_t max_pages = opt_.max_user_pages ? opt_.max_user_pages : kv_.device_pages;
+    if (uint64_t(max_users) * max_pages > (uint64_t(1) << 30)) {
+      err = "engine: device planner page table too large (set max_users / max_user_pages)";
+      return MTKV_ERROR;
+    }
+    if (ctl_.init(kv_.device_pages, kv_.page_size, kv_.chunk_size, opt_.mode == MTKV_MODE_HIERARCHICAL, max_users,
+                  max_pages, err))
+      return MTKV_ERROR;
+    planner.set_device_ctl(&ctl_);
+  }
   CK(cudaGetLastError());
   return MTKV_OK;
 }
@@ -308,7 +327,9 @@ static T* carve(char* base, size_t& off, size_t count) {
 int Engine::process_batch(const mtkv_request* reqs, uint32_t n, std::string& err) {
   CK(cudaSetDevice(opt_.device));
   BatchWork w;
+  const auto t0 = std::chrono::steady_clock::now();
   planner.plan_batch(reqs, n, w);
+  last_plan_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   const int rc = enqueue(w, reqs, n, err);
   if (w.rc) {
     err = w.error;
@@ -547,9 +568,16 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   const uint32_t* d_cid = d_creq + ncand_total;
   __nv_bfloat16* pool = static_cast<__nv_bfloat16*>(pool_.p);
 
+  const bool prof_copy = opt_.profile != 0;
+  if (prof_copy && !ev_copy_[0])
+    for (auto& e : ev_copy_) CK(cudaEventCreate(&e));
+  prof_scatter_ = prof_gather_ = 0;
   if (n_on) {
     CK(cudaStreamWaitEvent(comp_, ev_onload_[k], 0));
+    if (prof_copy) CK(cudaEventRecord(ev_copy_[0], comp_));
     launch_scatter_chunks(pool, static_cast<const __nv_bfloat16*>(staging_[sb].p), d_chunks, d_pages, n_on, g_, comp_);
+    if (prof_copy) CK(cudaEventRecord(ev_copy_[1], comp_));
+    prof_scatter_ = n_on;
     ++launches;
   }
   CK(cudaEventRecord(ev_scatter_[k], comp_));
@@ -672,7 +700,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
         waited = b;
       }
     }
+    if (prof_copy) CK(cudaEventRecord(ev_copy_[2], comp_));
     launch_gather_chunks(static_cast<__nv_bfloat16*>(offload_.p), pool, d_chunks + n_on, d_pages, n_off, g_, comp_);
+    if (prof_copy) CK(cudaEventRecord(ev_copy_[3], comp_));
+    prof_gather_ = n_off;
     ++launches;
     CK(cudaEventRecord(ev_gathered_[k], comp_));
     CK(cudaStreamWaitEvent(d2h_, ev_gathered_[k], 0));
@@ -844,6 +875,24 @@ double Engine::last_attention_ms(uint32_t* n) {
     tot += ms;
   }
   return tot;
+}
+
+int Engine::last_chunk_copy_ms(double* scatter_ms, uint32_t* scatter_chunks, double* gather_ms,
+                               uint32_t* gather_chunks) {
+  *scatter_ms = *gather_ms = 0;
+  *scatter_chunks = *gather_chunks = 0;
+  if (last_slot_ < 0 || !opt_.profile || !ev_copy_[0]) return MTKV_OK;
+  cudaEventSynchronize(ev_done_[last_slot_]);
+  float ms = 0;
+  if (prof_scatter_ && cudaEventElapsedTime(&ms, ev_copy_[0], ev_copy_[1]) == cudaSuccess) {
+    *scatter_ms = ms;
+    *scatter_chunks = prof_scatter_;
+  }
+  if (prof_gather_ && cudaEventElapsedTime(&ms, ev_copy_[2], ev_copy_[3]) == cudaSuccess) {
+    *gather_ms = ms;
+    *gather_chunks = prof_gather_;
+  }
+  return MTKV_OK;
 }
 
 void Engine::report(mtkv_run_report& r) const {

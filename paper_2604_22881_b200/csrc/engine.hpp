@@ -50,11 +50,19 @@ class Engine {
   // batches are in flight; valid for the last kRing submitted batches
   int batch_rankings(uint64_t ticket, uint32_t* out, uint64_t cap, std::string& err);
   uint64_t batches_submitted() const { return batch_no_; }
+  // wall time of the last batch's control plane (host planner, including the
+  // device planner's round trip when enabled) and the device planner kernel time
+  void last_plan_ms(double* plan_ms, double* ctl_kernel_ms) const {
+    *plan_ms = last_plan_ms_;
+    *ctl_kernel_ms = planner.device_ctl() ? ctl_.last_kernel_ms() : 0.0;
+  }
   int check_conservation(std::string& err);
   int64_t read_user_kv(uint32_t user, uint32_t layer, uint16_t* k, uint16_t* v, uint64_t cap,
                        std::string& err);
   double last_batch_ms();
   double last_attention_ms(uint32_t* launches);
+  // profile mode: device time of the last batch's onload scatter and offload gather
+  int last_chunk_copy_ms(double* scatter_ms, uint32_t* scatter_chunks, double* gather_ms, uint32_t* gather_chunks);
   void report(mtkv_run_report& r) const;
   void set_profile(uint32_t on) { opt_.profile = on; }
   uint32_t batch_size() const { return opt_.batch_size ? opt_.batch_size : 1; }
@@ -79,6 +87,8 @@ class Engine {
   cudaEvent_t ev_onload_[kRing], ev_scatter_[kRing], ev_gathered_[kRing], ev_d2h_[kRing],
       ev_done_[kRing], ev_start_[kRing];
   std::vector<cudaEvent_t> ev_attn_;  // profiling pairs of the last batch
+  cudaEvent_t ev_copy_[4] = {nullptr, nullptr, nullptr, nullptr};  // scatter start/end, gather start/end
+  uint32_t prof_scatter_ = 0, prof_gather_ = 0;
   uint32_t attn_launches_last_ = 0;
   uint64_t batch_no_ = 0;
   int64_t last_slot_ = -1;
@@ -93,6 +103,8 @@ class Engine {
   uint32_t staging_slots_ = 0;
   bool use_tc_ = false;          // tcgen05 attention (head_dim 64/128)
   int n_sm_ = 1;                 // persistent attention CTAs
+  DevCtl ctl_;                   // device control plane (opt_.device_planner)
+  double last_plan_ms_ = 0;
   AttnPlan plan_;                // attention plan of the batch being enqueued
   const char* trace_path_ = std::getenv("MTKV_ATTN_TRACE");
   DevBuf trace_;

@@ -103,7 +103,7 @@ struct AttnArgs {
   uint32_t bq;              // query rows per tile: 64 or 128 (items enumerate tiles of bq)
   unsigned long long* trace;  // optional per-CTA event timestamps (MTKV_ATTN_TRACE), else null
 };
-constexpr int kTraceCtas = 64, kTraceTiles = 32, kTraceKinds = 6;
+constexpr int kTraceCtas = 64, kTraceTiles = 96, kTraceKinds = 12;
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 
 struct GateArgs {  // split combine + silu(o) * u + layer norm -> bf16

@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include "devctl.hpp"
+
 namespace mtkv_b200 {
 
 static uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
@@ -66,7 +68,7 @@ uint32_t Planner::pop_page() {
 }
 
 void Planner::push_page(uint32_t p) {
-  free_.push_back(p);
+  if (!ctl_) free_.push_back(p);  // device mode: the free stack lives on the GPU
   --occupied_;
 }
 
@@ -90,6 +92,7 @@ bool Planner::evict_slot(int s, uint64_t* freed, std::string& err) {
 }
 
 int Planner::evict(uint32_t user, std::string& err) {
+  if (ctl_) { err = "evict: not available with the device planner (device tables own the pages)"; return MTKV_ERROR; }
   int s = slot_of(user, false);
   if (s < 0) { err = "evict: unknown user"; return MTKV_ERROR; }
   return evict_slot(s, nullptr, err) ? MTKV_OK : MTKV_ERROR;
@@ -130,6 +133,7 @@ void Planner::fire_completions(double now, std::vector<uint64_t>* persisted, Bat
     u.persisted_len += kv_.chunk_size;
     quota_used_ -= kv_.chunk_size;
     if (--u.pending == 0) u.locked = false;
+    note_update(p.slot);
     if (persisted) persisted->push_back(p.chunk_id);
   }
 }
@@ -189,6 +193,7 @@ void Planner::trigger_offloads(int s, double t, BatchWork& w) {
     const double done = schedule_offload(t);
     if (u.pending == 0) u.locked = true;
     ++u.pending;
+    note_update(s);
     pending_.push(Pending{done, order_++, s, ci, m.chunk_id});
   }
 }
@@ -207,7 +212,10 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
   w.reqs.resize(n);
   std::vector<uint32_t> scratch_ids;
 
-  if (cached) {
+  if (cached && ctl_) {
+    if (!prepare_on_device(reqs, n, slot, scratch_ids, w)) return;
+    st[0] = cost_.meta_fixed;
+  } else if (cached) {
     for (uint32_t i = 0; i < n; ++i) slot[i] = slot_of(reqs[i].user, true);
     std::vector<char> in_batch(users_.size(), 0);
     for (uint32_t i = 0; i < n; ++i) in_batch[slot[i]] = 1;
@@ -423,6 +431,101 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
   }
 }
 
+void Planner::note_update(int s) {
+  if (!ctl_) return;
+  const UserRec& u = users_[s];
+  const CtlUpd c{uint32_t(s), u.locked ? 1u : 0u, u.persisted_len};
+  auto it = ctl_upd_at_.find(s);
+  if (it != ctl_upd_at_.end()) ctl_upd_[it->second] = c;  // absolute values: latest wins
+  else {
+    ctl_upd_at_.emplace(s, ctl_upd_.size());
+    ctl_upd_.push_back(c);
+  }
+}
+
+// prepare_metadata (manager.cpp:74) with the decisions taken on the GPU: the
+// mirror applies slots, touches, evictions and page ids exactly as returned.
+bool Planner::prepare_on_device(const mtkv_request* reqs, uint32_t n, std::vector<int>& slot,
+                                std::vector<uint32_t>& scratch_ids, BatchWork& w) {
+  std::vector<CtlReq> cr(n);
+  for (uint32_t i = 0; i < n; ++i) cr[i] = CtlReq{reqs[i].user, reqs[i].new_token_count, reqs[i].candidate_count, 0};
+  std::string err;
+  const int rc = ctl_->prepare(cr.data(), n, ctl_upd_, err);
+  ctl_upd_.clear();
+  ctl_upd_at_.clear();
+  if (rc) {
+    w.rc = MTKV_ERROR;
+    w.error = err;
+    return false;
+  }
+  const CtlHdr& h = ctl_->hdr();
+  const CtlPlan* pl = ctl_->plans();
+  for (uint32_t i = 0; i < n; ++i) {
+    slot[i] = slot_of(reqs[i].user, true);
+    if (i < uint32_t(h.fail_at) && pl[i].slot != slot[i]) {
+      w.rc = MTKV_ERROR;
+      w.error = "device planner: slot numbering diverged from the host mirror";
+      return false;
+    }
+  }
+  const uint32_t touched = h.fail == CTL_OK ? n : uint32_t(h.fail_at) + 1;
+  for (uint32_t i = 0; i < touched && i < n; ++i) {
+    UserRec& u = users_[slot[i]];
+    u.known = true;
+    u.last_access = ++stamp_;
+    lru_front(slot[i]);
+  }
+  for (uint32_t e = 0; e < h.n_evict; ++e) {  // zero-copy evictions, in the device's order
+    const CtlEvict& ev = ctl_->evictions()[e];
+    UserRec& v = users_[ev.slot];
+    w.evictions.push_back(mtkv_eviction{v.id, ev.freed_pages, ev.tail_lost});
+    occupied_ -= v.pages.size();
+    v.pages.clear();
+    v.has_pages = false;
+    if (v.device_len > v.persisted_len) tail_lost_ += v.device_len - v.persisted_len;
+    v.device_len = 0;
+    ++evictions_;
+    lru_unlink(int(ev.slot));
+  }
+  const uint32_t allocated = std::min<uint32_t>(n, uint32_t(h.fail_at));
+  const uint32_t* ids = ctl_->ids();
+  for (uint32_t i = 0; i < allocated; ++i) {
+    const CtlPlan& c = pl[i];
+    mtkv_request_plan& p = w.reqs[i].plan;
+    p = mtkv_request_plan{};
+    p.user = reqs[i].user;
+    p.history_len = c.history_len;
+    p.delta = reqs[i].new_token_count;
+    p.num_candidates = reqs[i].candidate_count;
+    p.device_served = c.device_served;
+    p.host_onload = c.host_onload;
+    p.reusable_len = c.reusable_len;
+    p.onload_chunks = c.onload_chunks;
+    p.fresh_history = c.fresh_history;
+    UserRec& u = users_[slot[i]];
+    u.has_pages = true;
+    u.pages.insert(u.pages.end(), ids + c.grow_off, ids + c.grow_off + c.grow_n);
+    w.reqs[i].scratch_off = uint32_t(scratch_ids.size());
+    w.reqs[i].n_scratch = c.scratch_n;
+    scratch_ids.insert(scratch_ids.end(), ids + c.scratch_off, ids + c.scratch_off + c.scratch_n);
+    p.scratch_pages = c.scratch_n;
+    occupied_ += c.grow_n + c.scratch_n;
+    pages_allocated_ += c.grow_n + c.scratch_n;
+  }
+  if (h.fail != CTL_OK) {
+    if (h.fail == CTL_BAD_REQUEST) {
+      w.rc = MTKV_ERROR;
+      w.error = "request: need at least one candidate";
+    } else {
+      w.rc = MTKV_BATCH_REJECTED;
+      w.error = h.fail == CTL_REJECT_PAGES ? "batch exceeds total device pages"
+                                           : "allocation unsatisfiable: all resident users locked or in batch";
+    }
+    return false;
+  }
+  return true;
+}
+
 std::vector<uint32_t> Planner::known_users() const {
   std::vector<uint32_t> out;
   for (const auto& u : users_)
@@ -459,7 +562,7 @@ void Planner::report(mtkv_run_report& r) const {
   r.peak_pages = peak_pages_;
   r.pages_allocated = pages_allocated_;
   r.occupied_pages = occupied_;
-  r.free_pages = free_.size();
+  r.free_pages = kv_.device_pages - occupied_;
   r.quota_in_flight = quota_used_;
   r.clock = clock_;
   r.hist_required = required_;

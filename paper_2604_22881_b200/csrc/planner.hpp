@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/mtkv_b200.h"
+#include "devctl.hpp"
 
 namespace mtkv_b200 {
 
@@ -99,6 +100,10 @@ class Planner {
   int mode() const { return mode_; }
   uint32_t pages_per_chunk() const { return kv_.chunk_size / kv_.page_size; }
   uint64_t chunks_created() const { return next_chunk_id_; }
+  // Device control plane (devctl.hpp): prepare_metadata's decisions come from the
+  // GPU; this planner mirrors them and sends its own state changes back.
+  void set_device_ctl(DevCtl* c) { ctl_ = c; }
+  bool device_ctl() const { return ctl_ != nullptr; }
 
  private:
   int slot_of(uint32_t id, bool create);
@@ -108,6 +113,9 @@ class Planner {
   void push_page(uint32_t p);
   bool evict_slot(int s, uint64_t* freed, std::string& err);
   int free_pages_for(uint64_t need, const std::vector<char>& in_batch, BatchWork& w);
+  bool prepare_on_device(const mtkv_request* reqs, uint32_t n, std::vector<int>& slot,
+                         std::vector<uint32_t>& scratch_ids, BatchWork& w);
+  void note_update(int s);  // persisted length / lock bit changed on the host
   void fire_completions(double now, std::vector<uint64_t>* persisted, BatchWork* w);
   void schedule_onload(double submit, size_t n_chunks, std::vector<double>& fire);
   double schedule_offload(double submit);
@@ -151,6 +159,9 @@ class Planner {
   uint64_t required_ = 0, dev_served_ = 0, host_served_ = 0, processed_ = 0, requests_ = 0,
            batches_ = 0, peak_pages_ = 0;
   BatchWork last_;
+  DevCtl* ctl_ = nullptr;
+  std::vector<CtlUpd> ctl_upd_;  // host-side changes queued for the next device prepare
+  std::unordered_map<int, size_t> ctl_upd_at_;
 };
 
 }  // namespace mtkv_b200

@@ -58,6 +58,36 @@ def test_tag_engine_bit_exact(case):
         assert eng.kernel_launches() > 0
 
 
+@pytest.mark.parametrize("case", golden_cases("tag"), ids=lambda c: c["name"])
+def test_device_planner_bit_exact(case):
+    """GPU control plane (devctl.cu: batched lookup, LRU update, victim selection,
+    LIFO page allocation) reproduces the reference's complete control-plane
+    state digest after every batch, including rejected batches, and the data
+    it moves is byte-exact (conservation check)."""
+    ran = 0
+    for run in case["runs"]:
+        if run["mode"] == "recompute":
+            continue
+        eng = mtkv.Engine(_kv(case["kv"]), mode=run["mode"], backend="tag", batch_size=run["batch_size"],
+                          planner="device", max_users=4096)
+        for i, b in enumerate(batches(case["trace"], run["batch_size"])):
+            rej = False
+            try:
+                eng.process_batch(b)
+            except mtkv.BatchRejected:
+                rej = True
+            assert rej == run["rejected"][i], i
+            assert state_digest(eng.state()) == run["digests"][i], i
+        eng.drain()
+        eng.check_conservation()
+        assert eng.state() == run["final_state"]
+        rep = eng.report()
+        for k in REPORT_KEYS:
+            assert rep[k] == run["report"][k], k
+        ran += 1
+    assert ran > 0
+
+
 def _rel_logit_err(a, b):
     """max|a-b| relative to the row's logit scale (the reference model has no
     residual path, so logits are tiny, ~1e-8; bf16 keeps relative precision)."""
