@@ -234,6 +234,15 @@ int mtkv_op_gather_chunks(void* staging, const void* pool, const uint32_t* d_pag
 int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const uint32_t* d_pages,
                             uint32_t n_q, uint64_t p_pre, uint64_t n_keys, uint32_t layer,
                             const mtkv_kv_config* kv, uint32_t num_pages, void* stream);
+/* Batched form: request r's fresh rows (q rows [sum n_q[<r], +n_q[r])) attend over
+ * its p_pre[r] cached keys and themselves; its page ids start at
+ * d_pages[page_off[r]] (host arrays page_off / n_q / p_pre). repeat > 1 launches
+ * the attention kernel `repeat` times and returns the mean device ms of launches
+ * 2..repeat in *ms_per_launch (kernel benchmarking); out gets the merged result. */
+int mtkv_op_paged_attention_batch(float* out, const void* q, const void* pool, const uint32_t* d_pages,
+                                  const uint32_t* page_off, const uint32_t* n_q, const uint64_t* p_pre,
+                                  uint32_t n_req, uint32_t layer, const mtkv_kv_config* kv, uint32_t num_pages,
+                                  uint32_t repeat, float* ms_per_launch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -8,11 +8,13 @@
 //   warp 0      K producer: page-granular cp.async.bulk.tensor loads of K tiles
 //               straight out of the paged pool (no gather pass), NK-stage ring
 //   warp 3      V producer: same for V, NV-stage ring (V stays until PV, K is
-//               released as soon as S = Q K^T has been issued)
-//   warp 2      TMEM allocator, then Q loader (TMA, double-buffered per piece)
-//   warp 1      MMA issuer (one elected thread): S = Q K^T (A, B in smem) and
-//               O += P V (A = P in TMEM, B = V in smem) with tcgen05.mma
-//               kind::f16, fp32 accumulators in TMEM
+//               released as soon as S = Q K^T has completed)
+//   warp 1      MMA issuer (one elected lane): tcgen05.cp of the piece's Q into
+//               TMEM, S = Q K^T (A = Q in TMEM, B = K in smem) and O += P V
+//               (A = P in TMEM, B = V in smem) with tcgen05.mma kind::f16
+//   warp 2      TMEM allocator, then Q loader (TMA, double-buffered per piece; a
+//               buffer is refilled once its Q is in TMEM and the piece's
+//               epilogue, which stages O through it, is done)
 //   warps 4..11 two softmax pipelines (tiles of a piece alternate between
 //               them): thread r owns query row r (= TMEM lane r): tcgen05.ld of
 //               its S row, mask, online softmax in base 2, P -> TMEM (bf16x2,
@@ -24,7 +26,7 @@
 // Shared-memory operand layouts (canonical UMMA, 128-byte swizzle):
 //   Q, K : K-major  [rows][64-elem blocks], SBO = 1024 B, +32 B per K=16 step
 //   V    : MN-major [keys][64-dim blocks],  SBO = 1024 B, LBO = one block
-// TMEM columns per pipeline: S (64 fp32) | P (32 x bf16x2) | O (D fp32).
+// TMEM columns per pipeline: S (64 fp32) | P (32 x bf16x2) | O (D fp32); then Q (D/2).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -126,6 +128,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
   const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
   asm volatile(
@@ -155,6 +165,19 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 2^x for x <= 0 on the FMA pipe (Cody-Waite split + cubic minimax on [0,1),
+// max relative error 7.5e-5 << bf16 P rounding): a share of the exponentials
+// moves off the 16/clk/SM MUFU unit, which otherwise bounds the softmax.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.f);
+  const float fl = floorf(xc);
+  const float f = xc - fl;
+  const float p = fmaf(fmaf(fmaf(0.0780245001f, f, 0.2260672448f), f, 0.6958334771f), f, 0.9999252275f);
+  const float y = __int_as_float(__float_as_int(p) + (int(fl) << 23));
+  return x < -126.f ? 0.f : y;
+}
+constexpr int kPolyEvery = 4;  // every 4th column of a tile uses ex2_poly (0 = all MUFU)
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -191,6 +214,7 @@ struct TcCfg {
   static constexpr uint32_t TMEM_COLS = Q_COL + D / 2 <= 256 ? 256 : 512;
   static_assert(Q_COL + D / 2 <= 512, "TMEM budget");
   static constexpr size_t SMEM = 1024 + 2 * Q_BYTES + size_t(NK + NV) * T_BYTES + 256;
+  static_assert(8 * 32 * (D / 4) * 4 <= Q_BYTES, "epilogue staging fits one Q buffer");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -220,7 +244,7 @@ __global__ void __launch_bounds__(384, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                          // [2] Q buffers
+  uint8_t* sQ = smem;                          // [2] Q buffers (TMA target -> TMEM; then epilogue staging)
   uint8_t* sK = sQ + 2 * Q_BYTES;              // [NK] K tiles
   uint8_t* sV = sK + NK * T_BYTES;             // [NV] V tiles
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NV * T_BYTES);
@@ -233,8 +257,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_full = s_free + 2;    // [2] P in TMEM (+ O rescaled)
   uint64_t* o_done = p_full + 2;    // [2] PV completed
   uint64_t* q_full = o_done + 2;    // [2] Q buffer landed
-  uint64_t* q_empty = q_full + 2;   // [2] Q buffer's S MMAs completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 2);
+  uint64_t* q_empty = q_full + 2;   // [2] Q buffer copied into TMEM
+  uint64_t* epi_done = q_empty + 2; // [2] both pipelines' epilogues (staged in that Q buffer) done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 2);
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
@@ -252,6 +277,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&o_done[p], 1);
       mbar_init(&q_full[p], 1);
       mbar_init(&q_empty[p], 1);
+      mbar_init(&epi_done[p], 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -325,7 +351,10 @@ __global__ void __launch_bounds__(384, 1)
         const AttnSeg sg = a.segs[P.seg];
         const ReqDev R = a.reqs[sg.req];
         const uint32_t qb = k & 1;
-        if (k >= 2) mbar_wait(&q_empty[qb], ((k >> 1) - 1) & 1);
+        if (k >= 2) {
+          mbar_wait(&q_empty[qb], ((k >> 1) - 1) & 1);
+          mbar_wait(&epi_done[qb], ((k >> 1) - 1) & 1);  // piece k-2's epilogue staged in this buffer
+        }
         mbar_expect_tx(&q_full[qb], Q_BYTES);
 #pragma unroll
         for (int b = 0; b < NB; ++b)
@@ -335,8 +364,11 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: S(g+2) is issued before PV(g) ----------------
-    // Tiles alternate between the two softmax pipelines. The whole warp runs the (uniform) control flow so descriptor
-    // arithmetic stays on the uniform datapath; one elected lane issues.
+    // Tiles alternate between the two softmax pipelines; S of a pipeline's next
+    // tile only needs that pipeline to have loaded the previous S into registers,
+    // so it executes while the pipeline is still computing P. (Issuing S and PV
+    // from two different warps measured slower: 88 vs 65 us per launch.) The
+    // whole warp runs the uniform control flow; one elected lane issues.
     if (pe > pb) {
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
@@ -347,18 +379,19 @@ __global__ void __launch_bounds__(384, 1)
       cs.init(a, pb, pe);
       cv.init(a, pb, pe);
       auto issue_s = [&]() {
-        const uint32_t p = cs.j & 1, u = p ? cs.c1 : cs.c0, stk = cs.g % NK, qb = cs.k & 1;
+        const uint32_t p = cs.j & 1, u = p ? cs.c1 : cs.c0, stk = cs.g % NK;
         if (leader) ATTN_TR(9, cs.g);
         if (cs.j == 0) {
-          // new piece: copy its Q (landed by TMA) into TMEM, in order with the
-          // previous piece's S MMAs that still read the old Q
+          // new piece: copy its Q into TMEM, in order with the previous piece's
+          // S MMAs that still read the old Q
+          const uint32_t qb = cs.k & 1;
           mbar_wait(&q_full[qb], (cs.k >> 1) & 1);
           tc_after();
           if (leader) {
             const uint64_t aq = dq0 + ((qb * Q_BYTES) >> 4);
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
-              tmem_cp_128x256b(tmem + C::Q_COL + kk * 8, aq + (((kk / 4) * QBLK + (kk % 4) * 32) >> 4));
+              tmem_cp_128x256b(tmem + C::Q_COL + kk * 8, aq + ((((kk / 4) * QBLK + (kk % 4) * 32)) >> 4));
             mma_commit(&q_empty[qb]);  // smem Q buffer reusable once copied
           }
         }
@@ -378,13 +411,13 @@ __global__ void __launch_bounds__(384, 1)
         __syncwarp();
         cs.next(a);
       };
-      // S runs two tiles ahead of PV: S(g+2) only needs pipeline (g & 1) to have
-      // loaded S(g) into registers, so it executes while that pipeline is still
-      // computing P(g), and the pipeline finds its next S ready when it finishes.
-      issue_s();
-      if (cs.pc < pe) issue_s();
       while (cv.pc < pe) {
-        if (cs.pc < pe) issue_s();
+        // keep S up to two tiles ahead of PV; the first S of a new piece waits for
+        // that piece's Q and must not hold back the previous piece's last PVs
+        while (cs.pc < pe && cs.g < cv.g + 3) {
+          if (cs.j == 0 && cs.g > cv.g && !mbar_ready(&q_full[cs.k & 1], (cs.k >> 1) & 1)) break;
+          issue_s();
+        }
         const uint32_t p = cv.j & 1, u = p ? cv.c1 : cv.c0, stv = cv.g % NV;
         if (leader) ATTN_TR(10, cv.g);
         mbar_wait(&p_full[p], u & 1);
@@ -469,7 +502,8 @@ __global__ void __launch_bounds__(384, 1)
         float r4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
-          s[c] = ex2(fmaf(s[c], a.scale_log2, nmref));
+          const float x = fmaf(s[c], a.scale_log2, nmref);
+          s[c] = (kPolyEvery && c % kPolyEvery == kPolyEvery - 1) ? ex2_poly(x) : ex2(x);
           r4[c & 3] += s[c];
         }
         const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
@@ -515,21 +549,41 @@ __global__ void __launch_bounds__(384, 1)
       }
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const size_t prow = size_t(P.part + p) * BM + r;
-      float* dst = a.part_o + prow * D;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        float o[32];
-        if (mine > 0) {
-          tmem_ld32(o_col + c * 32, o);
+      if (mine > 0) {
+        // O/l -> HBM through a per-warp staging tile in this piece's (already
+        // copied) Q buffer: tcgen05.ld gives one row per thread, the staged
+        // tile is written back as whole 128-B row segments (coalesced)
+        constexpr int CW = D / 4;                 // staged columns per pass
+        constexpr int C4 = CW / 4;                // float4 chunks per staged row
+        const uint32_t kq = pc - pb, qb = kq & 1;
+        mbar_wait(&q_empty[qb], (kq >> 1) & 1);   // tcgen05.cp of this Q buffer finished
+        float* stg = reinterpret_cast<float*>(sQ + qb * Q_BYTES) + (warp - 4) * 32 * CW;
+        const uint32_t row0 = (warp % 4) * 32;    // first TMEM lane (query row) of this warp
+        float* dst_slot = a.part_o + size_t(P.part + p) * BM * D;
+#pragma unroll 1
+        for (int c = 0; c < D / CW; ++c) {
+          float o[32];
+          if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
+          else tmem_ld16(o_col + c * CW, o);
           tmem_wait_ld();
-        }
-        if (qi < q_end && mine > 0) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + i) = make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv);
+          for (int k = 0; k < C4; ++k)
+            *reinterpret_cast<float4*>(stg + lane * CW + ((k ^ (lane % C4)) << 2)) =
+                make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < C4; ++it) {
+            const uint32_t qd = lane + 32 * it, rr = qd / C4, k = qd % C4;
+            const float4 v = *reinterpret_cast<const float4*>(stg + rr * CW + ((k ^ (rr % C4)) << 2));
+            if (q0 + row0 + rr < q_end)
+              *reinterpret_cast<float4*>(dst_slot + size_t(row0 + rr) * D + c * CW + 4 * k) = v;
+          }
+          __syncwarp();
         }
       }
       if (qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
       if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
       tc_before();
     }

@@ -58,6 +58,10 @@ struct Smem {
   uint32_t prefix_bits, n_vict, fail, fail_at, i_end, fail_kind;
   uint64_t vkey[kMaxVictims];   // (stamp) of each victim
   uint32_t vslot[kMaxVictims];
+  uint32_t vnp[kMaxVictims];    // pages a victim frees
+  uint32_t vpos[kMaxVictims];   // stack position its first page is pushed to
+  uint32_t vreq[kMaxVictims];   // request whose ensure_free evicted it
+  uint32_t min_pos, max_pos, final_top, scratch_total;
 };
 
 __device__ uint64_t block_sum64(uint64_t v, Smem& sm) {
@@ -82,6 +86,12 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
   uint64_t* p_total = r_cum + a.n;  // projections, kept at a user's first occurrence
   uint64_t* p_dev = p_total + a.n;
   uint64_t* p_have = p_dev + a.n;
+  uint64_t* r_pers = p_have + a.n;   // persisted length (first occurrence)
+  uint32_t* r_first = reinterpret_cast<uint32_t*>(r_pers + a.n);
+  uint32_t* r_havei = r_first + a.n;  // pages the user holds before request i's grow
+  uint32_t* r_pop = r_havei + a.n;    // stack position of request i's lowest popped page
+  uint32_t* r_nv = r_pop + a.n;       // victims consumed up to and including request i
+  uint32_t* r_ids = r_nv + a.n;       // grow ids offset of request i
   const uint32_t tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   State& S = a.s;
   Globals& G = *S.g;
@@ -157,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     return;
   }
   const uint32_t epoch = G.epoch + 1;
-  // ---- 2. batch membership and first occurrence per user ----
+  // ---- 2. batch membership, first occurrence, per-request state into shared memory ----
   for (uint32_t i = tid; i < a.n; i += kThreads) S.firsti[r_slot[i]] = 0xFFFFFFFFu;
   __syncthreads();
   for (uint32_t i = tid; i < a.n; i += kThreads) {
@@ -165,34 +175,39 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     atomicMin(&S.firsti[r_slot[i]], i);
   }
   __syncthreads();
+  for (uint32_t i = tid; i < a.n; i += kThreads) {
+    const uint32_t s = r_slot[i], f = S.firsti[s];
+    r_first[i] = f;
+    if (f == i) {
+      p_total[i] = S.total[s];
+      p_dev[i] = S.dev[s];
+      p_have[i] = (S.flags[s] & F_HAS_PAGES) ? S.npages[s] : 0;
+      r_pers[i] = S.pers[s];
+    }
+  }
+  __syncthreads();
 
-  // ---- 3. plan numbers in request order (thread 0; a repeated user plans against the
-  //         projection its earlier occurrence left, manager.cpp:91-137) ----
+  // ---- 3. plan numbers in request order (thread 0, shared memory only; a repeated
+  //         user plans against its earlier occurrence's projection, manager.cpp:91-137) ----
   if (tid == 0) {
     G.epoch = epoch;
     uint64_t batch_need = 0;
     uint32_t fail_at = a.n, fail = CTL_OK;
     for (uint32_t i = 0; i < a.n; ++i) {
-      const uint32_t s = r_slot[i];
-      const uint32_t f = S.firsti[s];
-      if (f == i) {
-        p_total[i] = S.total[s];
-        p_dev[i] = S.dev[s];
-        p_have[i] = (S.flags[s] & F_HAS_PAGES) ? S.npages[s] : 0;
-      }
-      const uint64_t prior = p_total[f], devlen = p_dev[f], have = p_have[f];
+      const uint32_t f = r_first[i];
+      const uint64_t prior = p_total[f], devlen = p_dev[f], have = p_have[f], pers = r_pers[f];
       CtlPlan p{};
-      p.slot = int32_t(s);
+      p.slot = int32_t(r_slot[i]);
       p.history_len = prior;
       const uint32_t delta = a.reqs[i].delta, nc = a.reqs[i].ncand;
       if (nc < 1) { fail = CTL_BAD_REQUEST; fail_at = i; break; }
       if (devlen > 0) {
         p.device_served = devlen < prior ? devlen : prior;
         p.reusable_len = p.device_served;
-      } else if (a.hier && S.pers[s] > 0) {
-        p.host_onload = S.pers[s];
-        p.reusable_len = S.pers[s];
-        p.onload_chunks = uint32_t(S.pers[s] / a.chunk_size);
+      } else if (a.hier && pers > 0) {
+        p.host_onload = pers;
+        p.reusable_len = pers;
+        p.onload_chunks = uint32_t(pers / a.chunk_size);
       }
       p.fresh_history = prior - p.reusable_len;
       const uint64_t target = prior + delta;
@@ -204,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
       r_grow[i] = uint32_t(grow);
       r_scr[i] = uint32_t(scratch);
       r_cum[i] = batch_need;
+      r_havei[i] = uint32_t(have);
       a.plans[i] = p;
       p_total[f] = target;
       p_dev[f] = p.reusable_len + p.fresh_history + delta;
@@ -214,12 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
   }
   __syncthreads();
   // ---- 4. eviction victims: oldest stamps among in-list, unlocked, not-in-batch users ----
-  const uint32_t fail_at0 = sm.fail_at;
-  const uint32_t n_ok = fail_at0;  // requests whose allocation is attempted
+  const uint32_t n_ok = sm.fail_at;  // requests whose allocation is attempted
   const uint64_t free0 = G.top;
-  // total weight (pages) of eligible users
-  uint64_t wloc = 0;
   const uint32_t n_slots = G.n_slots;
+  uint64_t wloc = 0;
   for (uint32_t s = tid; s < n_slots; s += kThreads) {
     const uint32_t f = S.flags[s];
     if ((f & F_IN_LRU) && !(f & F_LOCKED) && S.mark[s] != epoch) wloc += (f & F_HAS_PAGES) ? S.npages[s] : 0;
@@ -249,18 +263,21 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     uint64_t thresh = ~uint64_t(0);
     if (need != ~uint64_t(0)) {
       // weighted radix select (8-bit digits, most significant first) of the stamp
-      // threshold tau = min{t : pages(eligible, stamp <= t) >= need}
+      // threshold tau = min{t : pages(eligible, stamp <= t) >= need}; leading
+      // all-zero digits of the largest stamp are skipped
+      int top_shift = 0;
+      for (uint64_t m = G.stamp >> 8; m; m >>= 8) top_shift += 8;
       uint64_t rem = need;
-      for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int shift = top_shift; shift >= 0; shift -= 8) {
         for (uint32_t b = tid; b < 256; b += kThreads) { sm.w_hist[b] = 0; sm.c_hist[b] = 0; }
         __syncthreads();
         const uint64_t pre = sm.prefix;
-        const uint32_t pbits = sm.prefix_bits;
+        const int hi = shift + 8;  // bits above this digit fixed by the prefix
         for (uint32_t s = tid; s < n_slots; s += kThreads) {
           const uint32_t f = S.flags[s];
           if (!((f & F_IN_LRU) && !(f & F_LOCKED) && S.mark[s] != epoch)) continue;
           const uint64_t st = S.last[s];
-          if (pbits && (st >> (64 - pbits)) != (pre >> (64 - pbits))) continue;
+          if (hi < 64 && (st >> hi) != (pre >> hi)) continue;
           const uint32_t dg = uint32_t(st >> shift) & 255u;
           atomicAdd(reinterpret_cast<unsigned long long*>(&sm.w_hist[dg]),
                     (unsigned long long)((f & F_HAS_PAGES) ? S.npages[s] : 0));
@@ -275,10 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
             if (acc + sm.w_hist[dg] >= rem) { dsel = dg; break; }
             acc += sm.w_hist[dg];
           }
-          rem -= acc;
           sm.prefix |= uint64_t(dsel) << shift;
-          sm.prefix_bits += 8;
-          sm.need = rem;
+          sm.need = rem - acc;
         }
         __syncthreads();
         rem = sm.need;
@@ -329,119 +344,134 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
         }
         __syncthreads();
       }
+    for (uint32_t k = tid; k < nv; k += kThreads) {
+      const uint32_t v = sm.vslot[k];
+      sm.vnp[k] = (S.flags[v] & F_HAS_PAGES) ? S.npages[v] : 0;
+    }
   }
   __syncthreads();
 
-  // ---- 5. touch + allocation walk in request order (warp 0): evict-push / pop ----
-  if (warp == 0) {
-    const uint32_t i_end = sm.i_end, fail = sm.fail, fail_at = sm.fail_at;
-    const uint32_t touch_end = fail == CTL_OK ? a.n : fail_at + 1;
-    uint64_t stamp = G.stamp;
-    uint32_t top = G.top, vi = 0, n_ev = 0, n_ids = 0;
-    const uint32_t nv = sm.n_vict;
+  // ---- 5. the interleaved evict-push / allocate-pop sequence of ensure_free + page
+  //         allocation (manager.cpp:55, :121-126), as stack positions (thread 0) ----
+  if (tid == 0) {
+    const uint32_t i_end = sm.i_end, nv = sm.n_vict;
+    uint32_t top = uint32_t(free0), vi = 0, ids = 0, lo = uint32_t(free0), hi = uint32_t(free0), scr = 0;
+    for (uint32_t i = 0; i < i_end; ++i) {
+      const uint32_t c = r_grow[i] + r_scr[i];
+      while (top < c && vi < nv) {
+        sm.vpos[vi] = top;
+        sm.vreq[vi] = i;
+        top += sm.vnp[vi++];
+      }
+      hi = max(hi, top);
+      top -= c;
+      r_pop[i] = top;
+      lo = min(lo, top);
+      r_nv[i] = vi;
+      r_ids[i] = ids;
+      ids += c;
+      scr += r_scr[i];
+    }
+    if (sm.fail == CTL_REJECT_VICTIMS)
+      for (; vi < nv; ++vi) {  // ensure_free of the failing request evicts everyone, then throws
+        sm.vpos[vi] = top;
+        sm.vreq[vi] = i_end;
+        top += sm.vnp[vi];
+        hi = max(hi, top);
+      }
+    sm.min_pos = lo;
+    sm.max_pos = hi;
+    sm.final_top = top;
+    sm.scratch_total = sm.fail == CTL_OK ? scr : 0;
+    sm.red32[0] = ids;
+    sm.red32[1] = vi;  // evictions
+  }
+  __syncthreads();
+  const uint32_t i_end = sm.i_end, n_ev = sm.red32[1], n_ids = sm.red32[0];
+  // value at stack position x as seen by request i's pops: the latest victim push
+  // (victims are ordered in time) covering x among those evicted up to request i,
+  // else the stack's content before the batch
+  auto stack_at = [&](uint32_t x, uint32_t nvic) -> uint32_t {
+    for (int k = int(nvic) - 1; k >= 0; --k)
+      if (x >= sm.vpos[k] && x < sm.vpos[k] + sm.vnp[k]) return S.ptab[size_t(sm.vslot[k]) * a.max_pages + (x - sm.vpos[k])];
+    return S.stack[x];
+  };
+  // pops of every allocating request, in parallel: grow pages (appended to the
+  // user's page list) then scratch pages; pop e of request i reads r_pop[i] + c_i - 1 - e
+  for (uint32_t i = warp; i < i_end; i += kThreads / 32) {
+    const uint32_t g = r_grow[i], c = g + r_scr[i], s = r_slot[i];
+    for (uint32_t e = lane; e < c; e += 32) {
+      const uint32_t pg = stack_at(r_pop[i] + c - 1 - e, r_nv[i]);
+      a.ids[r_ids[i] + e] = pg;
+      if (e < g) S.ptab[size_t(s) * a.max_pages + r_havei[i] + e] = pg;
+    }
+  }
+  // eviction records (state before the eviction)
+  for (uint32_t k = tid; k < n_ev; k += kThreads) {
+    const uint32_t v = sm.vslot[k];
+    const uint64_t dl = S.dev[v], pl = S.pers[v];
+    a.evict[k] = CtlEvict{v, 0, sm.vnp[k], 0, dl > pl ? dl - pl : 0};
+  }
+  __syncthreads();
+  // stack after the batch: positions [min_pos, final_top) take their last push;
+  // scratch pages are released on top in request order (manager.cpp:196)
+  const uint32_t lo = sm.min_pos, ftop = sm.final_top;
+  for (uint32_t x = lo + tid; x < ftop; x += kThreads) {
+    uint32_t val = kEmpty;
+    for (int k = int(n_ev) - 1; k >= 0; --k)
+      if (x >= sm.vpos[k] && x < sm.vpos[k] + sm.vnp[k]) { val = S.ptab[size_t(sm.vslot[k]) * a.max_pages + (x - sm.vpos[k])]; break; }
+    if (val != kEmpty) S.stack[x] = val;  // else unchanged since before the batch
+  }
+  __syncthreads();  // victim page lists are read above before they are cleared below
+  const uint32_t fail = sm.fail;
+  if (fail == CTL_OK) {
+    for (uint32_t i = warp; i < a.n; i += kThreads / 32) {
+      // scratch ids of request i go to ftop + (scratch released before it)
+      uint32_t before = 0;
+      for (uint32_t j = 0; j < i; ++j) before += r_scr[j];
+      const uint32_t c = r_grow[i] + r_scr[i];
+      for (uint32_t e = r_grow[i] + lane; e < c; e += 32) S.stack[ftop + before + (e - r_grow[i])] = a.ids[r_ids[i] + e];
+    }
+  }
+  for (uint32_t k = tid; k < n_ev; k += kThreads) {
+    const uint32_t v = sm.vslot[k];
+    S.npages[v] = 0;
+    S.flags[v] &= ~(F_HAS_PAGES | F_IN_LRU);
+    S.dev[v] = 0;
+  }
+  __syncthreads();
+  // ---- 6. touches (stamps in request order), page-list lengths, and on success the
+  //         end-of-batch commit_onload / finish_append (final projections) ----
+  if (tid == 0) {
+    const uint32_t touch_end = fail == CTL_OK ? a.n : sm.fail_at + 1;
+    const uint64_t stamp0 = G.stamp;
     for (uint32_t i = 0; i < touch_end && i < a.n; ++i) {
       const uint32_t s = r_slot[i];
-      ++stamp;
-      if (lane == 0) {
-        S.last[s] = stamp;
-        S.flags[s] |= F_KNOWN | F_IN_LRU;
-        if (i < a.n && i < fail_at) a.plans[i].stamp = stamp;
-      }
-      if (i >= i_end) {
-        if (fail == CTL_REJECT_VICTIMS && i == fail_at) {
-          // ensure_free evicts every eligible user, then throws
-          for (; vi < nv; ++vi) {
-            const uint32_t v = sm.vslot[vi];
-            const uint32_t np = (S.flags[v] & F_HAS_PAGES) ? S.npages[v] : 0;
-            for (uint32_t j = lane; j < np; j += 32) S.stack[top + j] = S.ptab[size_t(v) * a.max_pages + j];
-            __syncwarp();
-            if (lane == 0) {
-              const uint64_t dl = S.dev[v], pl = S.pers[v];
-              a.evict[n_ev] = CtlEvict{v, 0, np, 0, dl > pl ? dl - pl : 0};
-              S.npages[v] = 0;
-              S.flags[v] &= ~(F_HAS_PAGES | F_IN_LRU);
-              S.dev[v] = 0;
-            }
-            top += np;
-            ++n_ev;
-          }
-        }
-        continue;
-      }
-      const uint32_t grow = r_grow[i], scr = r_scr[i];
-      // ensure_free(grow + scratch): oldest eligible victims first
-      while (top < grow + scr && vi < nv) {
-        const uint32_t v = sm.vslot[vi++];
-        const uint32_t np = (S.flags[v] & F_HAS_PAGES) ? S.npages[v] : 0;
-        for (uint32_t j = lane; j < np; j += 32) S.stack[top + j] = S.ptab[size_t(v) * a.max_pages + j];
-        __syncwarp();
-        if (lane == 0) {
-          const uint64_t dl = S.dev[v], pl = S.pers[v];
-          a.evict[n_ev] = CtlEvict{v, 0, np, 0, dl > pl ? dl - pl : 0};
-          S.npages[v] = 0;
-          S.flags[v] &= ~(F_HAS_PAGES | F_IN_LRU);
-          S.dev[v] = 0;
-        }
-        top += np;
-        ++n_ev;
-      }
-      // pops: grow pages append to the user's list, then scratch pages
-      const uint32_t have = (S.flags[s] & F_HAS_PAGES) ? S.npages[s] : 0;
-      if (have + grow > a.max_pages) {
-        if (lane == 0) sm.fail = CTL_CAPACITY;
-        break;
-      }
-      for (uint32_t j = lane; j < grow; j += 32) {
-        const uint32_t pg = S.stack[top - 1 - j];
-        S.ptab[size_t(s) * a.max_pages + have + j] = pg;
-        a.ids[n_ids + j] = pg;
-      }
-      for (uint32_t j = lane; j < scr; j += 32) a.ids[n_ids + grow + j] = S.stack[top - grow - 1 - j];
-      __syncwarp();
-      if (lane == 0) {
-        a.plans[i].grow_off = n_ids;
-        a.plans[i].grow_n = grow;
-        a.plans[i].scratch_off = n_ids + grow;
-        a.plans[i].scratch_n = scr;
-        S.npages[s] = have + grow;
+      S.last[s] = stamp0 + i + 1;
+      S.flags[s] |= F_KNOWN | F_IN_LRU;
+      if (i < i_end) {
+        S.npages[s] = r_havei[i] + r_grow[i];  // last allocating occurrence wins
         S.flags[s] |= F_HAS_PAGES;
+        a.plans[i].stamp = stamp0 + i + 1;
+        a.plans[i].grow_off = r_ids[i];
+        a.plans[i].grow_n = r_grow[i];
+        a.plans[i].scratch_off = r_ids[i] + r_grow[i];
+        a.plans[i].scratch_n = r_scr[i];
       }
-      top -= grow + scr;
-      n_ids += grow + scr;
-      __syncwarp();
     }
-    if (lane == 0) {
-      G.stamp = stamp;
-      sm.fail_kind = n_ids;  // reuse: ids emitted
-      sm.red32[0] = top;
-      sm.red32[1] = n_ev;
-    }
+    G.stamp = stamp0 + min(touch_end, a.n);
   }
-  __syncthreads();
-  const uint32_t fail = sm.fail;
-  uint32_t top = sm.red32[0];
-  const uint32_t n_ids = sm.fail_kind, n_ev = sm.red32[1];
-  // ---- 6. end of batch: commit_onload, finish_append, release_scratch (request order) ----
-  if (fail == CTL_OK && tid == 0) {
-    for (uint32_t i = 0; i < a.n; ++i)
-      if (a.plans[i].onload_chunks > 0) S.dev[r_slot[i]] = a.plans[i].reusable_len;
-    for (uint32_t i = 0; i < a.n; ++i) {
-      const uint32_t s = r_slot[i];
-      S.dev[s] += a.plans[i].fresh_history + a.reqs[i].delta;
-      if (S.dev[s] > S.total[s]) S.total[s] = S.dev[s];
-    }
-  }
-  __syncthreads();
-  if (fail == CTL_OK && warp == 0) {
-    for (uint32_t i = 0; i < a.n; ++i) {
-      const uint32_t off = a.plans[i].scratch_off, ns = a.plans[i].scratch_n;
-      for (uint32_t j = lane; j < ns; j += 32) S.stack[top + j] = a.ids[off + j];
-      top += ns;
+  for (uint32_t i = tid; i < i_end; i += kThreads) {
+    if (r_first[i] != i) continue;
+    const uint32_t s = r_slot[i];
+    if (fail == CTL_OK) {
+      S.dev[s] = p_dev[i];
+      if (p_total[i] > S.total[s]) S.total[s] = p_total[i];
     }
   }
   __syncthreads();
   if (tid == 0) {
-    // evicted users' ids for the host mirror
+    const uint32_t top = fail == CTL_OK ? ftop + sm.scratch_total : ftop;
     G.top = top;
     CtlHdr h{};
     h.fail = int32_t(fail);
@@ -505,7 +535,7 @@ DevCtl::~DevCtl() {
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 int DevCtl::prepare(const CtlReq* reqs, uint32_t n, const std::vector<CtlUpd>& upd, std::string& err) {
-  const size_t smem = sizeof(Smem) + size_t(n) * 4 * 3 + 8 + size_t(n) * 8 * 4;
+  const size_t smem = sizeof(Smem) + size_t(n) * 4 * 3 + 8 + size_t(n) * 8 * 5 + size_t(n) * 4 * 5;
   if (smem > 200 * 1024) { err = "device planner: batch too large"; return -1; }
   // io layout: [reqs | upd | hdr | plans | evict (max_users) | ids (device_pages)]
   const size_t o_req = 0, o_upd = al(o_req + n * sizeof(CtlReq)), o_hdr = al(o_upd + upd.size() * sizeof(CtlUpd));

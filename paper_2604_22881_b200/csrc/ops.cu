@@ -1,8 +1,11 @@
 // Raw device ops of the C-ABI (kernel-level parity tests and integrations that
 // own their buffers): chunk scatter/gather and single-request paged attention.
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "kernels.cuh"
 #include "../../include/mtkv_b200.h"
@@ -58,13 +61,17 @@ static int chunk_op(bool to_pool, void* pool, void* staging, const uint32_t* d_p
   return finish(e);
 }
 
-// out[i][h*D + c] = log-sum-exp merge (base 2) of segment (h, i / bm)'s partial slots
-__global__ void merge_segs_kernel(float* out, const float* part, const float* lse, const AttnSeg* segs, uint32_t n_q,
-                                  uint32_t H, uint32_t D, uint32_t bm, uint32_t qtiles) {
+// out[row][h*D + c] = log-sum-exp merge (base 2) of the partial slots of the
+// row's segment (request, head, query tile)
+__global__ void merge_segs_kernel(float* out, const float* part, const float* lse, const AttnSeg* segs,
+                                  const ReqDev* reqs, const uint32_t* row_req, uint32_t rows, uint32_t H, uint32_t D,
+                                  uint32_t bm) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x, d = H * D;
-  if (idx >= n_q * d) return;
-  const uint32_t i = idx / d, j = idx % d, h = j / D, c = j % D, ri = i % bm;
-  const AttnSeg sg = segs[h * qtiles + i / bm];
+  if (idx >= rows * d) return;
+  const uint32_t row = idx / d, j = idx % d, h = j / D, c = j % D;
+  const ReqDev R = reqs[row_req[row]];
+  const uint32_t i = row - R.q_row0, ri = i % bm;
+  const AttnSeg sg = segs[R.seg0 + h * R.qtiles + i / bm];
   float m = -INFINITY;
   for (uint32_t k = 0; k < sg.n_parts; ++k) m = fmaxf(m, lse[size_t(sg.part_base + k) * bm + ri]);
   float num = 0.f, den = 0.f;
@@ -78,45 +85,40 @@ __global__ void merge_segs_kernel(float* out, const float* part, const float* ls
   out[idx] = den > 0.f ? num / den : 0.f;
 }
 
-extern "C" {
-
-int mtkv_op_scatter_chunks(void* pool, const void* staging, const uint32_t* d_page_ids, uint32_t n_chunks,
-                           const mtkv_kv_config* kv, uint32_t num_pages, void* stream) {
-  return chunk_op(true, pool, const_cast<void*>(staging), d_page_ids, n_chunks, kv, num_pages, stream);
-}
-
-int mtkv_op_gather_chunks(void* staging, const void* pool, const uint32_t* d_page_ids, uint32_t n_chunks,
-                          const mtkv_kv_config* kv, uint32_t num_pages, void* stream) {
-  return chunk_op(false, const_cast<void*>(pool), staging, d_page_ids, n_chunks, kv, num_pages, stream);
-}
-
-int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const uint32_t* d_pages, uint32_t n_q,
-                            uint64_t p_pre, uint64_t n_keys, uint32_t layer, const mtkv_kv_config* kv,
-                            uint32_t num_pages, void* stream) {
-  if (n_keys != p_pre + n_q) {
-    set_last_error("paged_attention: n_keys must equal p_pre + n_q");
-    return MTKV_ERROR;
-  }
-  if (!n_q) return MTKV_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+// Batched paged attention: request r's fresh rows [q_row0, q_row0 + n_q[r]) of q
+// attend over its p_pre[r] cached keys + themselves (causal); its page list
+// starts at d_pages[page_off[r]].
+static int attention_batch(float* out, const void* q, const void* pool, const uint32_t* d_pages,
+                           const uint32_t* page_off, const uint32_t* n_q, const uint64_t* p_pre, uint32_t n_req,
+                           uint32_t layer, const mtkv_kv_config* kv, uint32_t num_pages, uint32_t repeat,
+                           float* ms_per_launch, cudaStream_t s) {
   const PoolGeom g = geom(kv, num_pages);
-  ReqDev r{};
-  r.q_row0 = 0;
-  r.n_q = n_q;
-  r.n_hist = n_q;
-  r.n_cand = 0;
-  r.start = p_pre;
-  r.pages_off = 0;
-  r.n_pages = uint32_t((n_keys + g.S - 1) / g.S);
+  std::vector<ReqDev> rq(n_req);
+  uint32_t rows = 0;
+  for (uint32_t r = 0; r < n_req; ++r) {
+    ReqDev& x = rq[r];
+    x = ReqDev{};
+    x.q_row0 = rows;
+    x.n_q = x.n_hist = n_q[r];
+    x.start = p_pre[r];
+    x.pages_off = page_off[r];
+    x.n_pages = uint32_t((p_pre[r] + n_q[r] + g.S - 1) / g.S);
+    rows += n_q[r];
+  }
+  if (!rows) return MTKV_OK;
+  std::vector<uint32_t> row_req(rows);
+  for (uint32_t r = 0; r < n_req; ++r)
+    for (uint32_t i = 0; i < n_q[r]; ++i) row_req[rq[r].q_row0 + i] = r;
   const char* force = std::getenv("MTKV_ATTN");
   const bool tc = attn_tc_supported(g) && !(force && std::string(force) == "mma");
   AttnPlan plan;
-  plan_attention(&r, 1, g, tc, tc ? uint32_t(num_sms()) : 0, plan);
+  plan_attention(rq.data(), n_req, g, tc, tc ? uint32_t(num_sms()) : 0, plan);
   const uint32_t n_items = tc ? plan.n_ctas() : uint32_t(plan.items.size());
-  // one device allocation: request | segments | items or pieces + CTA offsets | lse | partials
+  // one device allocation: requests | rows | segments | items or pieces + CTA offsets | lse | partials
   size_t off = 0;
   auto carve = [&](size_t bytes) { const size_t o = off; off = (off + bytes + 255) & ~size_t(255); return o; };
-  const size_t o_req = carve(sizeof(ReqDev));
+  const size_t o_req = carve(rq.size() * sizeof(ReqDev));
+  const size_t o_rr = carve(row_req.size() * sizeof(uint32_t));
   const size_t o_seg = carve(plan.segs.size() * sizeof(AttnSeg));
   const size_t o_items = carve(plan.items.size() * sizeof(AttnItem));
   const size_t o_pieces = carve(plan.pieces.size() * sizeof(AttnPiece));
@@ -129,7 +131,8 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   auto up = [&](size_t o, const void* src, size_t bytes) {
     if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(buf + o, src, bytes, cudaMemcpyHostToDevice, s);
   };
-  up(o_req, &r, sizeof(r));
+  up(o_req, rq.data(), rq.size() * sizeof(ReqDev));
+  up(o_rr, row_req.data(), row_req.size() * sizeof(uint32_t));
   up(o_seg, plan.segs.data(), plan.segs.size() * sizeof(AttnSeg));
   up(o_items, plan.items.data(), plan.items.size() * sizeof(AttnItem));
   up(o_pieces, plan.pieces.data(), plan.pieces.size() * sizeof(AttnPiece));
@@ -152,22 +155,88 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
   a.bq = plan.bm;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
   if (e == cudaSuccess) {
-    if (tc) {
-      alignas(64) CUtensorMap pmap, qmap;
-      if (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, n_q, g)) {
-        cudaFreeAsync(buf, s);
-        set_last_error("paged_attention: cuTensorMapEncodeTiled failed");
-        return MTKV_ERROR;
-      }
-      launch_attention_tc(pmap, qmap, a, s);
-    } else {
-      launch_attention(a, s);
+    alignas(64) CUtensorMap pmap, qmap;
+    if (tc && (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, rows, g))) {
+      cudaFreeAsync(buf, s);
+      set_last_error("paged_attention: cuTensorMapEncodeTiled failed");
+      return MTKV_ERROR;
     }
-    merge_segs_kernel<<<(n_q * g.d + 255) / 256, 256, 0, s>>>(out, a.part_o, a.part_lse, a.segs, n_q, g.H, g.D,
-                                                               plan.bm, r.qtiles);
+    // MTKV_ATTN_TRACE=<file>: per-CTA event timelines of the last launch (tools/attn_trace.py)
+    const char* trace_path = tc ? std::getenv("MTKV_ATTN_TRACE") : nullptr;
+    unsigned long long* trace = nullptr;
+    const size_t trace_bytes = size_t(kTraceCtas) * kTraceKinds * kTraceTiles * 8;
+    if (trace_path && cudaMallocAsync((void**)&trace, trace_bytes, s) == cudaSuccess) {
+      cudaMemsetAsync(trace, 0, trace_bytes, s);
+      a.trace = trace;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (repeat > 1 && ms_per_launch) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+    }
+    for (uint32_t it = 0; it < std::max<uint32_t>(repeat, 1); ++it) {
+      if (it == 1 && e0) cudaEventRecord(e0, s);  // first launch is the warm-up
+      if (tc) launch_attention_tc(pmap, qmap, a, s);
+      else launch_attention(a, s);
+    }
+    if (e0) {
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      *ms_per_launch = ms / float(repeat - 1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    if (trace) {
+      std::vector<unsigned long long> h(trace_bytes / 8);
+      cudaMemcpyAsync(h.data(), trace, trace_bytes, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      if (FILE* f = std::fopen(trace_path, "wb")) {
+        std::fwrite(h.data(), 8, h.size(), f);
+        std::fclose(f);
+      }
+      cudaFreeAsync(trace, s);
+    }
+    merge_segs_kernel<<<(rows * g.d + 255) / 256, 256, 0, s>>>(out, a.part_o, a.part_lse, a.segs, a.reqs,
+                                                                reinterpret_cast<const uint32_t*>(buf + o_rr), rows,
+                                                                g.H, g.D, plan.bm);
   }
   cudaFreeAsync(buf, s);
   return finish(e);
+}
+
+extern "C" {
+
+int mtkv_op_scatter_chunks(void* pool, const void* staging, const uint32_t* d_page_ids, uint32_t n_chunks,
+                           const mtkv_kv_config* kv, uint32_t num_pages, void* stream) {
+  return chunk_op(true, pool, const_cast<void*>(staging), d_page_ids, n_chunks, kv, num_pages, stream);
+}
+
+int mtkv_op_gather_chunks(void* staging, const void* pool, const uint32_t* d_page_ids, uint32_t n_chunks,
+                          const mtkv_kv_config* kv, uint32_t num_pages, void* stream) {
+  return chunk_op(false, const_cast<void*>(pool), staging, d_page_ids, n_chunks, kv, num_pages, stream);
+}
+
+int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const uint32_t* d_pages, uint32_t n_q,
+                            uint64_t p_pre, uint64_t n_keys, uint32_t layer, const mtkv_kv_config* kv,
+                            uint32_t num_pages, void* stream) {
+  if (n_keys != p_pre + n_q) {
+    set_last_error("paged_attention: n_keys must equal p_pre + n_q");
+    return MTKV_ERROR;
+  }
+  if (!n_q) return MTKV_OK;
+  const uint32_t zero = 0;
+  return attention_batch(out, q, pool, d_pages, &zero, &n_q, &p_pre, 1, layer, kv, num_pages, 1, nullptr,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int mtkv_op_paged_attention_batch(float* out, const void* q, const void* pool, const uint32_t* d_pages,
+                                  const uint32_t* page_off, const uint32_t* n_q, const uint64_t* p_pre, uint32_t n_req,
+                                  uint32_t layer, const mtkv_kv_config* kv, uint32_t num_pages, uint32_t repeat,
+                                  float* ms_per_launch, void* stream) {
+  return attention_batch(out, q, pool, d_pages, page_off, n_q, p_pre, n_req, layer, kv, num_pages, repeat,
+                         ms_per_launch, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

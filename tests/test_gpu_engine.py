@@ -259,6 +259,47 @@ def test_paged_attention_op_vs_torch_fp32(H, D, S, p_pre, n_q):
     assert err <= ATTN_TOL
 
 
+def test_paged_attention_batch_op_vs_torch_fp32():
+    """Batched op (the persistent kernel's real work mix): several requests with
+    different prefixes / fresh-row counts (1 and 2 query tiles) in one launch."""
+    H, D, S, L, layer = 2, 128, 32, 2, 1
+    d = H * D
+    p_pre = np.array([4100, 0, 777, 2048, 33], dtype=np.uint64)
+    n_q = np.array([72, 199, 129, 1, 64], dtype=np.uint32)
+    pages_per = ((p_pre + n_q + S - 1) // S).astype(np.int64)
+    P = int(pages_per.sum()) + 9
+    pool = _paged_pool(L, P, S, d, seed=5)
+    pages = torch.randperm(P, device="cuda").to(torch.int32)
+    page_off = np.concatenate([[0], np.cumsum(pages_per)[:-1]]).astype(np.uint32)
+    rows = int(n_q.sum())
+    q = (torch.randn(rows, d, device="cuda") * 0.5).to(torch.bfloat16)
+    out = torch.empty(rows, d, device="cuda", dtype=torch.float32)
+    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=S, chunk_size=S, device_pages=P))
+    u32p = lambda a: a.ctypes.data_as(mtkv.C.POINTER(mtkv.C.c_uint32))
+    rc = mtkv.lib().mtkv_op_paged_attention_batch(
+        out.data_ptr(), q.data_ptr(), pool.data_ptr(), pages.data_ptr(), u32p(page_off), u32p(n_q),
+        p_pre.ctypes.data_as(mtkv.C.POINTER(mtkv.C.c_uint64)), len(n_q), layer, mtkv.C.byref(kv._c()), P, 1, None,
+        torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, mtkv._err()
+    torch.cuda.synchronize()
+    worst, r0 = 0.0, 0
+    for r in range(len(n_q)):
+        nk = int(p_pre[r] + n_q[r])
+        pg = pages[int(page_off[r]):int(page_off[r]) + int(pages_per[r])].long()
+        K = pool[layer, pg, 0].reshape(-1, d)[:nk].float()
+        V = pool[layer, pg, 1].reshape(-1, d)[:nk].float()
+        qf = q[r0:r0 + int(n_q[r])].float()
+        pos = torch.arange(int(n_q[r]), device="cuda") + int(p_pre[r])
+        mask = torch.arange(nk, device="cuda")[None, :] <= pos[:, None]
+        for h in range(H):
+            sc = (qf[:, h * D:(h + 1) * D] @ K[:, h * D:(h + 1) * D].T / D ** 0.5).masked_fill(~mask, float("-inf"))
+            ref = torch.softmax(sc, dim=-1) @ V[:, h * D:(h + 1) * D]
+            worst = max(worst, (out[r0:r0 + int(n_q[r]), h * D:(h + 1) * D] - ref).abs().max().item())
+        r0 += int(n_q[r])
+    print(f"attention batch op: max abs err {worst:.2e}")
+    assert worst <= ATTN_TOL
+
+
 def test_scatter_gather_round_trip_bit_exact():
     L, H, D, S, chunk, P = 3, 2, 64, 32, 128, 40
     d = H * D

@@ -1,0 +1,69 @@
+"""Attention kernel microbenchmark on the bench layer's shape (one layer, one batch).
+
+64 requests, 4 K-token cached prefixes (+ up to 16 earlier revisits), d=256 (H=2, D=128),
+page 32; fresh rows per request = 64 new + 8 candidates, plus the lost tail
+(0..127 rows) for the ~69 % of requests that were onloaded from the host tier
+(the bench's steady-state mix). Pages are a random permutation of a 40 K-page pool
+(no locality). Times `repeat` back-to-back launches with CUDA events and reports
+algorithmic GB/s against MEASURED_PEAKS.json (same accounting as bench.py).
+
+  python tools/attn_bench.py [--repeat 50] [--seed 0] [--tag name]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2604_22881_b200 as mtkv  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--repeat", type=int, default=50)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--tag", default="")
+    ap.add_argument("--requests", type=int, default=64)
+    args = ap.parse_args()
+    rng = np.random.default_rng(args.seed)
+    L, H, D, S = 4, 2, 128, 32
+    d = H * D
+    n = args.requests
+    p_pre = (4096 + 64 * rng.integers(0, 16, n)).astype(np.uint64)
+    tail = np.where(rng.random(n) < 0.69, rng.integers(0, 128, n), 0)
+    n_q = (72 + tail).astype(np.uint32)
+    pages_per = ((p_pre + n_q + S - 1) // S).astype(np.int64)
+    P = int(pages_per.sum() + 64)
+    perm = rng.permutation(P).astype(np.int32)
+    page_off = np.concatenate([[0], np.cumsum(pages_per)[:-1]]).astype(np.uint32)
+    pool = (torch.randn(L, P, 2, S, d, device="cuda") * 0.5).to(torch.bfloat16)
+    pages = torch.from_numpy(perm).cuda()
+    rows = int(n_q.sum())
+    q = (torch.randn(rows, d, device="cuda") * 0.5).to(torch.bfloat16)
+    out = torch.empty(rows, d, device="cuda", dtype=torch.float32)
+    kv = mtkv.KVConfig(num_layers=L, num_heads=H, head_dim=D, page_size=S, chunk_size=128, device_pages=P)
+    ms = mtkv.C.c_float(0)
+    u32p = lambda a: a.ctypes.data_as(mtkv.C.POINTER(mtkv.C.c_uint32))
+    rc = mtkv.lib().mtkv_op_paged_attention_batch(
+        out.data_ptr(), q.data_ptr(), pool.data_ptr(), pages.data_ptr(), u32p(page_off), u32p(n_q),
+        p_pre.ctypes.data_as(mtkv.C.POINTER(mtkv.C.c_uint64)), n, 1, mtkv.C.byref(kv._c()), P, args.repeat,
+        mtkv.C.byref(ms), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, mtkv._err()
+    torch.cuda.synchronize()
+    keys = p_pre + n_q
+    nbytes = int((keys * d * 4).sum() + (n_q.astype(np.int64) * d * 6).sum())
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    gbs = nbytes / (ms.value / 1e3) / 1e9
+    print(json.dumps({"tag": args.tag, "us_per_launch": ms.value * 1e3, "bytes_per_launch": nbytes,
+                      "rows": rows, "two_tile_requests": int((n_q > 128).sum()), "GBs": gbs, "peak": peak,
+                      "frac": gbs / peak, "env": {k: v for k, v in os.environ.items() if k.startswith("MTKV_")}}))
+
+
+if __name__ == "__main__":
+    main()
