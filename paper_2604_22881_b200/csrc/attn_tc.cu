@@ -110,6 +110,29 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// predicated forms: every lane of a uniform warp executes the instruction, only
+// `on` issues it (no divergent branch around the tensor-core issue)
+__device__ __forceinline__ void mma_ts_if(bool on, uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(uint32_t(on))
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_if(bool on, uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.b32 q, %1, 0;\n"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(s32(bar)),
+      "r"(uint32_t(on))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_cp_if(bool on, uint32_t taddr, uint64_t sdesc_) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(taddr),
+      "l"(sdesc_), "r"(uint32_t(on))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc_) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc_) : "memory");
 }
@@ -191,7 +214,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define ATTN_TR(kind, t)                                                                  \
   do {                                                                                    \
-    if (a.trace && blockIdx.x < kTraceCtas && (t) < kTraceTiles)                          \
+    if (TR && blockIdx.x < kTraceCtas && (t) < kTraceTiles)                               \
       a.trace[((size_t)blockIdx.x * kTraceKinds + (kind)) * kTraceTiles + (t)] = gtime(); \
   } while (0)
 
@@ -218,23 +241,8 @@ struct TcCfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-struct TileCursor {  // walks a CTA's pieces tile by tile
-  uint32_t pc, end, t, lo, hi, j, g, k, c0, c1;  // c0/c1: tiles issued per pipeline
-  __device__ void init(const AttnArgs& a, uint32_t b, uint32_t e) {
-    pc = b; end = e; g = 0; k = 0; j = 0; c0 = c1 = 0;
-    load(a);
-  }
-  __device__ void load(const AttnArgs& a) {
-    if (pc < end) { const AttnPiece P = a.pieces[pc]; lo = P.lo; hi = P.hi; t = lo; }
-  }
-  __device__ void next(const AttnArgs& a) {
-    if (j & 1) ++c1; else ++c0;
-    ++g; ++t; ++j;
-    if (t == hi) { ++pc; ++k; j = 0; load(a); }
-  }
-};
 
-template <int D>
+template <int D, bool TR>  // TR: per-CTA event trace (MTKV_ATTN_TRACE builds only)
 __global__ void __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map, AttnArgs a) {
   using C = TcCfg<D>;
@@ -268,8 +276,11 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) ATTN_TR(5, 0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 1); }
-    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 1); }
+    // a stage is released by the 4 warps of the softmax pipeline that owns the
+    // tile: K once they have loaded S (so S, hence the K read, completed), V once
+    // they have seen that tile's PV complete (keeps commits off the MMA thread)
+    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 4); }
+    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 4); }
     for (int p = 0; p < 2; ++p) {
       mbar_init(&s_full[p], 1);
       mbar_init(&s_free[p], 4);
@@ -368,73 +379,91 @@ __global__ void __launch_bounds__(384, 1)
     // tile only needs that pipeline to have loaded the previous S into registers,
     // so it executes while the pipeline is still computing P. (Issuing S and PV
     // from two different warps measured slower: 88 vs 65 us per launch.) The
-    // whole warp runs the uniform control flow; one elected lane issues.
+    // whole warp runs branch-free uniform code: stage / phase counters advance
+    // incrementally and one elected lane issues through predicated instructions.
     if (pe > pb) {
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
           (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       const uint64_t dq0 = sdesc(s32(sQ), 16, 1024), dk0 = sdesc(s32(sK), 16, 1024), dv0 = sdesc(s32(sV), KBLK, 1024);
       const bool leader = elect_one();
-      TileCursor cs, cv;
-      cs.init(a, pb, pe);
-      cv.init(a, pb, pe);
+      // S cursor: piece, tiles left in it, tile-in-piece, pieces seen, K stage/phase, S tiles per pipeline
+      uint32_t s_pc = pb, s_left = 0, s_j = 0, s_k = 0, stk = 0, phk = 0, s_cnt0 = 0, s_cnt1 = 0, s_g = 0;
+      // PV cursor
+      uint32_t v_pc = pb, v_left = 0, v_j = 0, stv = 0, phv = 0, pph = 0 /* bit p: phase of p_full[p] */, v_g = 0;
+      uint32_t total = 0;
+      for (uint32_t pc = pb; pc < pe; ++pc) total += a.pieces[pc].hi - a.pieces[pc].lo;
+      {
+        const AttnPiece P0 = a.pieces[pb];
+        s_left = v_left = P0.hi - P0.lo;
+      }
       auto issue_s = [&]() {
-        const uint32_t p = cs.j & 1, u = p ? cs.c1 : cs.c0, stk = cs.g % NK;
-        if (leader) ATTN_TR(9, cs.g);
-        if (cs.j == 0) {
+        const uint32_t p = s_j & 1;
+        ATTN_TR(9, s_g);
+        if (s_j == 0) {
           // new piece: copy its Q into TMEM, in order with the previous piece's
           // S MMAs that still read the old Q
-          const uint32_t qb = cs.k & 1;
-          mbar_wait(&q_full[qb], (cs.k >> 1) & 1);
+          const uint32_t qb = s_k & 1;
+          mbar_wait(&q_full[qb], (s_k >> 1) & 1);
           tc_after();
-          if (leader) {
-            const uint64_t aq = dq0 + ((qb * Q_BYTES) >> 4);
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              tmem_cp_128x256b(tmem + C::Q_COL + kk * 8, aq + ((((kk / 4) * QBLK + (kk % 4) * 32)) >> 4));
-            mma_commit(&q_empty[qb]);  // smem Q buffer reusable once copied
-          }
-        }
-        if (u > 0) mbar_wait(&s_free[p], (u - 1) & 1);
-        mbar_wait(&full_k[stk], (cs.g / NK) & 1);
-        tc_after();
-        if (leader) {
-          const uint64_t bk = dk0 + ((stk * T_BYTES) >> 4);
-          const uint32_t d_tmem = tmem + p * C::PIPE + C::S_COL;
+          const uint64_t aq = dq0 + ((qb * Q_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            mma_ts(d_tmem, tmem + C::Q_COL + kk * 8, bk + (((kk / 4) * KBLK + (kk % 4) * 32) >> 4), idesc_s, kk > 0);
-          mma_commit(&s_full[p]);
-          mma_commit(&empty_k[stk]);
-          ATTN_TR(1, cs.g);
+            tmem_cp_if(leader, tmem + C::Q_COL + kk * 8, aq + ((((kk / 4) * QBLK + (kk % 4) * 32)) >> 4));
+          mma_commit_if(leader, &q_empty[qb]);  // smem Q buffer reusable once copied
         }
-        __syncwarp();
-        cs.next(a);
+        const uint32_t cnt = p ? s_cnt1 : s_cnt0;  // S tiles this pipeline already got
+        if (cnt > 0) mbar_wait(&s_free[p], (cnt - 1) & 1);
+        mbar_wait(&full_k[stk], phk);
+        tc_after();
+        const uint64_t bk = dk0 + ((stk * T_BYTES) >> 4);
+        const uint32_t d_tmem = tmem + p * C::PIPE + C::S_COL;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ts_if(leader, d_tmem, tmem + C::Q_COL + kk * 8, bk + (((kk / 4) * KBLK + (kk % 4) * 32) >> 4), idesc_s,
+                    kk > 0);
+        mma_commit_if(leader, &s_full[p]);
+        if (leader) ATTN_TR(1, s_g);
+        // advance
+        if (p) ++s_cnt1; else ++s_cnt0;
+        if (++stk == NK) { stk = 0; phk ^= 1; }
+        ++s_g;
+        ++s_j;
+        if (--s_left == 0) {
+          ++s_pc;
+          ++s_k;
+          s_j = 0;
+          if (s_pc < pe) { const AttnPiece Pn = a.pieces[s_pc]; s_left = Pn.hi - Pn.lo; }
+        }
       };
-      while (cv.pc < pe) {
+      for (uint32_t g = 0; g < total; ++g) {
         // keep S up to two tiles ahead of PV; the first S of a new piece waits for
         // that piece's Q and must not hold back the previous piece's last PVs
-        while (cs.pc < pe && cs.g < cv.g + 3) {
-          if (cs.j == 0 && cs.g > cv.g && !mbar_ready(&q_full[cs.k & 1], (cs.k >> 1) & 1)) break;
+        while (s_g < total && s_g < g + 3) {
+          if (s_j == 0 && s_g > g && !mbar_ready(&q_full[s_k & 1], (s_k >> 1) & 1)) break;
           issue_s();
         }
-        const uint32_t p = cv.j & 1, u = p ? cv.c1 : cv.c0, stv = cv.g % NV;
-        if (leader) ATTN_TR(10, cv.g);
-        mbar_wait(&p_full[p], u & 1);
-        mbar_wait(&full_v[stv], (cv.g / NV) & 1);
+        const uint32_t p = v_j & 1;
+        ATTN_TR(10, v_g);
+        mbar_wait(&p_full[p], (pph >> p) & 1);
+        mbar_wait(&full_v[stv], phv);
         tc_after();
-        if (leader) {
-          const uint64_t bv = dv0 + ((stv * T_BYTES) >> 4);
-          const uint32_t d_tmem = tmem + p * C::PIPE + C::O_COL, a_tmem = tmem + p * C::PIPE + C::P_COL;
+        const uint64_t bv = dv0 + ((stv * T_BYTES) >> 4);
+        const uint32_t d_tmem = tmem + p * C::PIPE + C::O_COL, a_tmem = tmem + p * C::PIPE + C::P_COL;
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            mma_ts(d_tmem, a_tmem + kk * 8, bv + ((kk * 2048) >> 4), idesc_o, (cv.j >= 2 || kk > 0) ? 1u : 0u);
-          mma_commit(&o_done[p]);
-          mma_commit(&empty_v[stv]);
-          ATTN_TR(2, cv.g);
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_ts_if(leader, d_tmem, a_tmem + kk * 8, bv + ((kk * 2048) >> 4), idesc_o, (v_j >= 2 || kk > 0) ? 1u : 0u);
+        mma_commit_if(leader, &o_done[p]);
+        if (leader) ATTN_TR(2, v_g);
+        pph ^= 1u << p;
+        if (++stv == NV) { stv = 0; phv ^= 1; }
+        ++v_g;
+        ++v_j;
+        if (--v_left == 0) {
+          ++v_pc;
+          v_j = 0;
+          if (v_pc < pe) { const AttnPiece Pn = a.pieces[v_pc]; v_left = Pn.hi - Pn.lo; }
         }
-        __syncwarp();
-        cv.next(a);
       }
     }
   } else if (warp >= 4) {
@@ -445,7 +474,15 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t s_col = tmem + lane_base + p * C::PIPE + C::S_COL;
     const uint32_t p_col = tmem + lane_base + p * C::PIPE + C::P_COL;
     const uint32_t o_col = tmem + lane_base + p * C::PIPE + C::O_COL;
-    uint32_t u = 0;  // tiles this pipeline has processed (barrier phases)
+    uint32_t u = 0;          // tiles this pipeline has processed (barrier phases)
+    uint32_t gbase = 0;      // CTA-wide index of the current piece's first tile
+    int32_t pend_v = -1;     // tile whose V stage this pipeline still has to release
+    auto release_v = [&]() {
+      if (pend_v >= 0) {
+        if (lane == 0) mbar_arrive(&empty_v[uint32_t(pend_v) % NV]);
+        pend_v = -1;
+      }
+    };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const AttnSeg sg = a.segs[P.seg];
@@ -479,7 +516,10 @@ __global__ void __launch_bounds__(384, 1)
         if (threadIdx.x % 128 == 0) ATTN_TR(6, u * 2 + p);
         tc_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[p]);
+        if (lane == 0) {
+          mbar_arrive(&s_free[p]);
+          mbar_arrive(&empty_k[(gbase + t - P.lo) % NK]);
+        }
         const int kb = int(t - P.lo) * BN;
         const int cu = min(max(ue - kb, 0), BN), c_lo = min(max(cl - kb, 0), BN), c_hi = min(max(ce - kb, 0), BN);
         if (cu != BN) {
@@ -512,6 +552,7 @@ __global__ void __launch_bounds__(384, 1)
         if (u > 0) {  // this pipeline's previous PV must finish before P / O are touched
           mbar_wait(&o_done[p], (u - 1) & 1);
           tc_after();
+          release_v();
         }
         if (threadIdx.x % 128 == 0) ATTN_TR(8, u * 2 + p);
         // P -> TMEM in two halves (keeps the live register set small), then the lazy O rescale
@@ -537,6 +578,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[p]);
+        pend_v = int32_t(gbase + t - P.lo);
         if (threadIdx.x % 128 == 0) ATTN_TR(4, u * 2 + p);
         if (threadIdx.x % 128 == 96) ATTN_TR(11, u * 2 + p);
       }
@@ -546,6 +588,7 @@ __global__ void __launch_bounds__(384, 1)
       if (mine > 0) {
         mbar_wait(&o_done[p], (u - 1) & 1);
         tc_after();
+        release_v();
       }
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       const size_t prow = size_t(P.part + p) * BM + r;
@@ -584,6 +627,7 @@ __global__ void __launch_bounds__(384, 1)
       if (qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
       __syncwarp();
       if (lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
+      gbase += P.hi - P.lo;
       if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
       tc_before();
     }
@@ -643,10 +687,12 @@ template <int D>
 static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
+    cudaFuncSetAttribute(attn_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
+    cudaFuncSetAttribute(attn_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
     set = true;
   }
-  attn_tc_kernel<D><<<a.n_items, 384, TcCfg<D>::SMEM, s>>>(pool_map, q_map, a);
+  if (a.trace) attn_tc_kernel<D, true><<<a.n_items, 384, TcCfg<D>::SMEM, s>>>(pool_map, q_map, a);
+  else attn_tc_kernel<D, false><<<a.n_items, 384, TcCfg<D>::SMEM, s>>>(pool_map, q_map, a);
 }
 
 void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
