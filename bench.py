@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "requests/sec & tokens/sec at fixed hit ratio, p99 latency, 1/2/4/8 B200 vs CPU"
+H2D_PEAK_GBS = 55.5  # measured pinned H2D, 64-256 MiB copies (profiles/r01_probe_h2d.json)
 
 CONFIGS = {
     # BASELINE.json configs[1] — the headline single-GPU workload
@@ -304,6 +305,11 @@ def run_b200(args, cfg):
             dist.destroy_process_group()
         return
     avg_launch_s = (attn_ms / 1e3) / max(attn_launches, 1)
+    # DRAM traffic of one attention launch from the committed ncu capture (profiles/)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("traffic_bytes_per_launch")
     achieved = (attn_bytes / max(attn_launches, 1)) / avg_launch_s / 1e9 if attn_launches else 0.0
     line = {
         "metric": METRIC,
@@ -336,12 +342,19 @@ def run_b200(args, cfg):
         "gpu_launches": int(round(launches_per_step * K)),
         "gpu_launches_per_step": launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
+                     "traffic_source": "profiles/attn_traffic.json (ncu --set full, dram read+write bytes per launch)",
                      "kernel": "attn_tc_kernel (tcgen05 paged incremental attention)",
                      "launches_timed": attn_launches,
                      "avg_launch_us": avg_launch_s * 1e6,
                      "bytes_per_launch": attn_bytes / max(attn_launches, 1)},
         "clocks": clk,
+        # host link (north star: H2D GB/s against the measured pinned-copy peak,
+        # tools/probe_h2d.py: 55.5 GB/s for >= 64 MiB copies on this pool's B200 boxes)
+        "host_link": {"h2d_GBs": phase_a["h2d_bytes_per_step"] * K / elapsed / 1e9, "peak_GBs": H2D_PEAK_GBS,
+                      "frac": phase_a["h2d_bytes_per_step"] * K / elapsed / 1e9 / H2D_PEAK_GBS,
+                      "d2h_GBs": phase_a["d2h_bytes_per_step"] * K / elapsed / 1e9,
+                      "note": "timed phase A; the step is host-link bound when frac ~ 1"},
         "control_plane": {"planner": args.planner,
                           "plan_ms_per_batch": float(np.mean(plan_ms)) if plan_ms else None,
                           "device_planner_kernel_us": float(np.mean(ctl_ms)) * 1e3 if args.planner == "device" else None,

@@ -324,6 +324,24 @@ static T* carve(char* base, size_t& off, size_t count) {
   return p;
 }
 
+// dense layers: tcgen05 kernel (gemm_tc.cu) for every shape it covers, mma.sync
+// otherwise; MTKV_GEMM=mma forces the legacy kernel for A/B measurements
+int Engine::gemm(const GemmArgs& a, uint64_t a_rows_alloc, std::string& err) {
+  static const bool force_mma = [] {
+    const char* f = std::getenv("MTKV_GEMM");
+    return f && std::string(f) == "mma";
+  }();
+  if (!force_mma && gemm_tc_supported(a)) {
+    if (launch_gemm_tc(a, a_rows_alloc, comp_)) {
+      err = "engine: cuTensorMapEncodeTiled (GEMM operands) failed";
+      return MTKV_ERROR;
+    }
+  } else {
+    launch_gemm(a, comp_);
+  }
+  return MTKV_OK;
+}
+
 int Engine::process_batch(const mtkv_request* reqs, uint32_t n, std::string& err) {
   CK(cudaSetDevice(opt_.device));
   BatchWork w;
@@ -612,7 +630,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       ga.A = X; ga.B = w_in_ + size_t(l) * d * 4 * d; ga.M = rows; ga.N = 4 * d; ga.K = d;
       ga.epi = Epi::Proj; ga.out_u = U; ga.out_q = Q; ga.pool = pool; ga.kv_off = d_kv;
       ga.layer_base = size_t(l) * g_.num_pages * 2 * S * d; ga.d = d; ga.kv_stride = S * d;
-      launch_gemm(ga, comp_);
+      if (gemm(ga, x_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       AttnArgs aa{};
       aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.segs = d_segs; aa.items = d_items;
       aa.n_items = n_items; aa.pieces = d_pieces; aa.cta_off = d_ctaoff;
@@ -653,10 +671,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       launch_gate_norm(gn, comp_);
       GemmArgs m1{};
       m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = rows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID;
-      launch_gemm(m1, comp_);
+      if (gemm(m1, x2_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       GemmArgs m2{};
       m2.A = MID; m2.B = w2_ + size_t(l) * d * d; m2.M = rows; m2.N = d; m2.K = d; m2.epi = Epi::Bf16; m2.out = X;
-      launch_gemm(m2, comp_);
+      if (gemm(m2, mid_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       launches += 5;
     }
     GemmArgs hd{};

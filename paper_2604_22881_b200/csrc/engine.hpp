@@ -61,6 +61,7 @@ class Engine {
                        std::string& err);
   double last_batch_ms();
   double last_attention_ms(uint32_t* launches);
+  int gemm(const GemmArgs& a, uint64_t a_rows_alloc, std::string& err);
   // profile mode: device time of the last batch's onload scatter and offload gather
   int last_chunk_copy_ms(double* scatter_ms, uint32_t* scatter_chunks, double* gather_ms, uint32_t* gather_chunks);
   void report(mtkv_run_report& r) const;

@@ -1,0 +1,273 @@
+// Dense layers of the GR block on the 5th-gen tensor cores (sm_100a):
+// C[M x N] = A[M x K] . W[K x N] with bf16 operands, fp32 accumulation in TMEM,
+// and the epilogues of the reference block (model.cpp:171-196) fused:
+//   Proj     : silu, then u | q -> bf16 activations, k | v -> appended straight
+//              into the paged KV pool at each fresh row's (page, slot)
+//              (the north-star "KV append/write-back" of the new tokens)
+//   SiluBf16 : silu -> bf16 (MLP up)
+//   Bf16     : bf16 (MLP down)
+// One CTA per 128 x BN output tile (128 threads): warp 0 streams A / W k-blocks
+// with TMA (128-B swizzle, 4-stage ring), one elected lane of warp 1 issues
+// tcgen05.mma kind::f16 (A K-major, W MN-major), all 4 warps drain TMEM
+// (tcgen05.ld, one output row per thread) through the fused epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace mtkv_b200 {
+
+namespace gtc {
+
+constexpr int BM = 128, BK = 64, NSTG = 4;
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          s32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+}  // namespace gtc
+
+using namespace gtc;
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap w_map, GemmArgs g) {
+  constexpr uint32_t A_BYTES = BM * BK * 2;       // 16 KB: 128 rows x 64 k
+  constexpr uint32_t W_BYTES = BK * BN * 2;       // 64 k rows x BN cols (BN / 64 boxes of 8 KB)
+  constexpr uint32_t STG = A_BYTES + W_BYTES;
+  constexpr uint32_t TCOLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTG * STG);
+  uint64_t* empty = full + NSTG;
+  uint64_t* done = empty + NSTG;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (g.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tslot)), "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NSTG;
+      if (kb >= NSTG) mbar_wait(&empty[st], ((kb / NSTG) - 1) & 1);
+      mbar_expect_tx(&full[st], STG);
+      uint8_t* sa = smem + st * STG;
+      tma_load_2d(sa, &a_map, kb * BK, m0, &full[st]);
+#pragma unroll
+      for (int b = 0; b < BN / 64; ++b) tma_load_2d(sa + A_BYTES + b * (BK * 128), &w_map, n0 + 64 * b, kb * BK, &full[st]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc =
+        (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NSTG;
+      mbar_wait(&full[st], (kb / NSTG) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sa = s32(smem + st * STG), sw = sa + A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk)
+        mma_ss(tmem, sdesc(sa + kk * 32, 16, 1024), sdesc(sw + kk * 2048, BK * 128, 1024), idesc,
+               (kb > 0 || kk > 0) ? 1u : 0u);
+      commit(&empty[st]);
+    }
+    commit(done);
+  }
+  // epilogue: thread t owns output row m0 + t (TMEM lane t)
+  __syncwarp();
+  mbar_wait(done, 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + int(threadIdx.x);
+  const uint32_t taddr = tmem + ((32u * warp) << 16);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float v[32];
+    tmem_ld32(taddr + c * 32, v);
+    if (row >= g.M) continue;
+    const int col0 = n0 + c * 32;
+    if (g.epi == Epi::Proj) {
+      // the 32 columns lie in one of u | q | k | v when d % 32 == 0
+      const uint32_t part = uint32_t(col0) / g.d, w = uint32_t(col0) % g.d;
+      __nv_bfloat16* dst = part == 0   ? g.out_u + size_t(row) * g.d + w
+                           : part == 1 ? g.out_q + size_t(row) * g.d + w
+                                       : g.pool + g.layer_base + g.kv_off[row] + (part == 3 ? g.kv_stride : 0) + w;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(silu(v[i]), silu(v[i + 1]));
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(silu(v[i + 2]), silu(v[i + 3]));
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(silu(v[i + 4]), silu(v[i + 5]));
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(silu(v[i + 6]), silu(v[i + 7]));
+        pk.x = *reinterpret_cast<uint32_t*>(&h0);
+        pk.y = *reinterpret_cast<uint32_t*>(&h1);
+        pk.z = *reinterpret_cast<uint32_t*>(&h2);
+        pk.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(dst + i) = pk;
+      }
+    } else {
+      const bool act = g.epi == Epi::SiluBf16;
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.out) + size_t(row) * g.N + col0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 pk;
+        float x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = act ? silu(v[i + j]) : v[i + j];
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]), h1 = __floats2bfloat162_rn(x[2], x[3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(x[4], x[5]), h3 = __floats2bfloat162_rn(x[6], x[7]);
+        pk.x = *reinterpret_cast<uint32_t*>(&h0);
+        pk.y = *reinterpret_cast<uint32_t*>(&h1);
+        pk.z = *reinterpret_cast<uint32_t*>(&h2);
+        pk.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(dst + i) = pk;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+}
+
+// ------------------------------------------------------------------ host ---
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_g() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&fn), cudaEnableDefault, &q);
+  }
+  return fn;
+}
+
+static bool encode(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                   uint32_t box_rows) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cuuint64_t(cols) * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  auto fn = encode_fn_g();
+  return fn && fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool gemm_tc_supported(const GemmArgs& a) {
+  return !a.row_idx && a.epi != Epi::F32 && a.K % 64 == 0 && a.N % 64 == 0 && (a.epi != Epi::Proj || a.d % 32 == 0);
+}
+
+template <int BN>
+static void launch_bn(const CUtensorMap& am, const CUtensorMap& wm, const GemmArgs& a, cudaStream_t s) {
+  constexpr size_t smem = 1024 + NSTG * (BM * BK * 2 + BK * BN * 2) + 128;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set = true;
+  }
+  const dim3 grid(a.N / BN, (a.M + BM - 1) / BM);
+  gemm_tc_kernel<BN><<<grid, 128, smem, s>>>(am, wm, a);
+}
+
+// tensor maps are cached per (buffer, shape, box): activation workspaces and
+// weights are long-lived, so steady-state batches encode nothing
+struct MapKey {
+  const void* p;
+  uint64_t cols, rows;
+  uint32_t bc, br;
+  bool operator==(const MapKey& o) const {
+    return p == o.p && cols == o.cols && rows == o.rows && bc == o.bc && br == o.br;
+  }
+};
+static const CUtensorMap* cached_map(const void* base, uint64_t cols, uint64_t rows, uint32_t bc, uint32_t br) {
+  struct Entry {
+    MapKey k;
+    alignas(64) CUtensorMap m;
+  };
+  static thread_local std::vector<Entry> cache;
+  const MapKey k{base, cols, rows, bc, br};
+  for (const Entry& e : cache)
+    if (e.k == k) return &e.m;
+  if (cache.size() >= 64) cache.erase(cache.begin());
+  cache.emplace_back();
+  cache.back().k = k;
+  if (!encode(&cache.back().m, base, cols, rows, bc, br)) {
+    cache.pop_back();
+    return nullptr;
+  }
+  return &cache.back().m;
+}
+
+// A: [M x K] activations (rows padded by TMA zero fill), W: [K x N] row-major weights
+int launch_gemm_tc(const GemmArgs& a, uint64_t a_rows_alloc, cudaStream_t s) {
+  if (a.M <= 0) return 0;
+  const CUtensorMap* amp = cached_map(a.A, a.K, a_rows_alloc, BK, BM);
+  const CUtensorMap* wmp = cached_map(a.B, a.N, a.K, 64, BK);
+  if (!amp || !wmp) return -1;
+  const CUtensorMap am = *amp, wm = *wmp;
+  // wide N: 128-column tiles; narrow N (MLP, d): 64-column tiles for more CTAs
+  if (a.N >= 1024) launch_bn<128>(am, wm, a, s);
+  else launch_bn<64>(am, wm, a, s);
+  return 0;
+}
+
+}  // namespace mtkv_b200

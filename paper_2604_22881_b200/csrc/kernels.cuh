@@ -82,6 +82,9 @@ struct GemmArgs {
 };
 
 void launch_gemm(const GemmArgs& a, cudaStream_t s);
+// tcgen05 path (gemm_tc.cu): Proj / SiluBf16 / Bf16 epilogues, K and N multiples of 64
+bool gemm_tc_supported(const GemmArgs& a);
+int launch_gemm_tc(const GemmArgs& a, uint64_t a_rows_alloc, cudaStream_t s);
 void launch_embed(__nv_bfloat16* x, const __nv_bfloat16* table, const uint32_t* tok, int rows, int d,
                   cudaStream_t s);
 
