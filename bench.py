@@ -44,10 +44,14 @@ CONFIGS = {
     # configs[0] — the reference's smallest CPU case (parity-test sized)
     "tiny_d64": dict(L=2, H=2, D=32, vocab=512, users=256, history=1024, delta=32, cands=8,
                      page=32, chunk=128, pool_frac=0.10, batch=32),
-    # configs[3] per GPU shard — production-scale model
-    "gr8_d512": dict(L=8, H=4, D=128, vocab=4096, users=1024, history=8192, delta=64, cands=8,
-                     page=32, chunk=128, pool_frac=0.10, batch=32),
+    # configs[3] per GPU shard — production-scale model (8-layer d=512, 8K histories);
+    # 256 users per GPU keep the pinned host tier at ~35 GB per process
+    "gr8_d512": dict(L=8, H=4, D=128, vocab=4096, users=256, history=8192, delta=64, cands=8,
+                     page=32, chunk=128, pool_frac=0.10, batch=16),
 }
+
+
+CONFIG_TAG = {"gr4_d256": "configs[1]", "tiny_d64": "configs[0]", "gr8_d512": "configs[3]"}
 
 
 def dist_env():
@@ -324,7 +328,7 @@ def run_b200(args, cfg):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random token ids, reference-initialised random weights)",
-        "config": {"workload": f"configs[1] {args.config}: {cfg['L']} layers d={cfg['H'] * cfg['D']}, "
+        "config": {"workload": f"{CONFIG_TAG[args.config]} {args.config}: {cfg['L']} layers d={cfg['H'] * cfg['D']}, "
                                f"{cfg['history']}-token histories, {cfg['delta']} new + {cfg['cands']} "
                                f"candidates/request, HBM pool {int(cfg['pool_frac'] * 100)}% of users, "
                                f"pinned-host tier, hierarchical",
@@ -406,7 +410,7 @@ def run_reference(args, cfg):
     line = {"metric": METRIC, "value": base["value"], "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"configs[1] {args.config} (reference CPU serving path, sampled)"},
+            "config": {"workload": f"{CONFIG_TAG[args.config]} {args.config} (reference CPU serving path, sampled)"},
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "requests/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}

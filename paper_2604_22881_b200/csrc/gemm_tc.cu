@@ -7,7 +7,7 @@
 //   SiluBf16 : silu -> bf16 (MLP up)
 //   Bf16     : bf16 (MLP down)
 // One CTA per 128 x BN output tile (128 threads): warp 0 streams A / W k-blocks
-// with TMA (128-B swizzle, 4-stage ring), one elected lane of warp 1 issues
+// with TMA (128-B swizzle, 2-stage ring; several CTAs per SM), one elected lane of warp 1 issues
 // tcgen05.mma kind::f16 (A K-major, W MN-major), all 4 warps drain TMEM
 // (tcgen05.ld, one output row per thread) through the fused epilogue.
 #include <cuda.h>
@@ -21,7 +21,7 @@ namespace mtkv_b200 {
 
 namespace gtc {
 
-constexpr int BM = 128, BK = 64, NSTG = 4;
+constexpr int BM = 128, BK = 64, NSTG = 2;  // 2 stages: 3-4 CTAs per SM overlap one tile's epilogue with others' loads
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
@@ -78,7 +78,7 @@ __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x));
 using namespace gtc;
 
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap w_map, GemmArgs g) {
   constexpr uint32_t A_BYTES = BM * BK * 2;       // 16 KB: 128 rows x 64 k
   constexpr uint32_t W_BYTES = BK * BN * 2;       // 64 k rows x BN cols (BN / 64 boxes of 8 KB)
