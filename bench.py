@@ -18,6 +18,17 @@ engine, then W revisit batches. Timed: K revisit batches. Synthetic data
 N > 1: launched by torchrun, one process per GPU; users are sharded by
 user id (u -> u*N + rank), each rank owns an independent cache shard; no
 collective on the data path ("scaling": "weak").
+
+Phases: A = device throughput (`value`, pre-packed requests, CUDA events);
+B = per-batch latency (p50/p99) with per-kernel CUDA-event timing of the
+attention launches (`roofline`) and the KV scatter/gather (`other_kernels`);
+C = end to end through the public API (`e2e`: Python request dicts -> C-ABI,
+pipelined submit / rankings read-back of every batch). Also reported:
+`host_link` (H2D GB/s vs the measured pinned-copy peak), `control_plane`
+(planning cost; `--planner device` runs the GPU control plane), `cpu_baseline`
+(the unmodified reference on this box's host cores). Other BASELINE configs:
+`--config gr8_d512` (configs[3] per-GPU shard), `tools/sweep.py ablation|pressure`
+(configs[2], configs[4]).
 """
 from __future__ import annotations
 

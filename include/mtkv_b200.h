@@ -243,6 +243,13 @@ int mtkv_op_paged_attention_batch(float* out, const void* q, const void* pool, c
                                   const uint32_t* page_off, const uint32_t* n_q, const uint64_t* p_pre,
                                   uint32_t n_req, uint32_t layer, const mtkv_kv_config* kv, uint32_t num_pages,
                                   uint32_t repeat, float* ms_per_launch, void* stream);
+/* Host-only self-check of the attention work planner (attn_plan.cpp): plans a
+ * batch (fresh history rows, candidates and cached prefix per request) for
+ * `ctas` persistent CTAs and verifies every (request, head, query tile, key
+ * tile) is covered exactly once and partial slots are contiguous. Returns 0 or
+ * a failure code; out_stats[5] = {segments, pieces, tiles, max tiles per CTA, CTAs}. */
+int mtkv_attention_plan_check(uint32_t n, const uint32_t* n_hist, const uint32_t* n_cand, const uint64_t* start,
+                              uint32_t H, uint32_t D, uint32_t S, uint32_t ctas, int tc, uint32_t* out_stats);
 
 #ifdef __cplusplus
 }

@@ -135,7 +135,7 @@ EXPORTED_SYMBOLS = [
     "mtkv_user_pages", "mtkv_lru_snapshot", "mtkv_evict_user", "mtkv_is_locked",
     "mtkv_get_total_cache_length", "mtkv_gen_config_default", "mtkv_gen_config_preset",
     "mtkv_generate_trace_jsonl", "mtkv_free", "mtkv_op_scatter_chunks", "mtkv_op_gather_chunks",
-    "mtkv_op_paged_attention", "mtkv_op_paged_attention_batch",
+    "mtkv_op_paged_attention", "mtkv_op_paged_attention_batch", "mtkv_attention_plan_check",
 ]
 
 _lib = None
@@ -201,6 +201,8 @@ def lib():
         "mtkv_op_gather_chunks": (C.c_int, [vp, vp, vp, u32, C.POINTER(_KV), u32, vp]),
         "mtkv_op_paged_attention": (C.c_int, [vp, vp, vp, vp, u32, u64, u64, u32, C.POINTER(_KV),
                                               u32, vp]),
+        "mtkv_attention_plan_check": (C.c_int, [u32, u32p, u32p, C.POINTER(C.c_uint64), u32, u32, u32, u32, C.c_int,
+                                                u32p]),
         "mtkv_op_paged_attention_batch": (C.c_int, [vp, vp, vp, vp, u32p, u32p, C.POINTER(C.c_uint64), u32, u32,
                                                     C.POINTER(_KV), u32, u32, C.POINTER(C.c_float), vp]),
     }

@@ -149,3 +149,74 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
 }
 
 }  // namespace mtkv_b200
+
+// ---- C-ABI self-check of the planner (host only; used by the CPU tests) ----
+#include "../../include/mtkv_b200.h"
+
+extern "C" int mtkv_attention_plan_check(uint32_t n, const uint32_t* n_hist, const uint32_t* n_cand,
+                                         const uint64_t* start, uint32_t H, uint32_t D, uint32_t S, uint32_t ctas,
+                                         int tc, uint32_t* out_stats) {
+  using namespace mtkv_b200;
+  PoolGeom g{};
+  g.H = H;
+  g.D = D;
+  g.d = H * D;
+  g.S = S;
+  g.L = 1;
+  std::vector<ReqDev> rq(n);
+  uint32_t rows = 0;
+  for (uint32_t r = 0; r < n; ++r) {
+    rq[r] = ReqDev{};
+    rq[r].q_row0 = rows;
+    rq[r].n_hist = n_hist[r];
+    rq[r].n_cand = n_cand[r];
+    rq[r].n_q = n_hist[r] + n_cand[r];
+    rq[r].start = start[r];
+    rows += rq[r].n_q;
+  }
+  AttnPlan P;
+  plan_attention(rq.data(), n, g, tc != 0, ctas, P);
+  // every segment: its slots are contiguous and its tiles are covered exactly once
+  std::vector<std::vector<uint32_t>> cover(P.segs.size());
+  for (size_t s = 0; s < P.segs.size(); ++s) cover[s].assign(tc ? P.segs[s].n_tiles : 1, 0);
+  uint64_t tiles = 0, max_cta = 0;
+  if (tc) {
+    if (P.cta_off.empty() || P.cta_off.front() != 0 || P.cta_off.back() != P.pieces.size()) return 1;
+    for (size_t c = 0; c + 1 < P.cta_off.size(); ++c) {
+      uint64_t t = 0;
+      for (uint32_t i = P.cta_off[c]; i < P.cta_off[c + 1]; ++i) {
+        const AttnPiece& pc = P.pieces[i];
+        if (pc.seg >= P.segs.size() || pc.lo >= pc.hi || pc.hi > P.segs[pc.seg].n_tiles) return 2;
+        const AttnSeg& sg = P.segs[pc.seg];
+        if (pc.part < sg.part_base || pc.part + 2 > sg.part_base + sg.n_parts) return 3;
+        for (uint32_t x = pc.lo; x < pc.hi; ++x) ++cover[pc.seg][x];
+        t += pc.hi - pc.lo;
+      }
+      tiles += t;
+      max_cta = std::max(max_cta, t);
+    }
+    for (auto& cv : cover)
+      for (uint32_t c : cv)
+        if (c != 1) return 4;
+  } else {
+    for (const AttnItem& it : P.items) {
+      const ReqDev& R = rq[it.req];
+      const uint32_t sg = R.seg0 + it.head * R.qtiles + it.qtile;
+      if (sg >= P.segs.size() || it.split >= P.segs[sg].n_parts) return 5;
+    }
+  }
+  uint32_t slots = 0;
+  for (const AttnSeg& sg : P.segs) {
+    if (sg.part_base != slots) return 6;  // contiguous, in segment order
+    slots += sg.n_parts;
+  }
+  if (slots != P.n_slots) return 7;
+  if (out_stats) {
+    out_stats[0] = uint32_t(P.segs.size());
+    out_stats[1] = uint32_t(tc ? P.pieces.size() : P.items.size());
+    out_stats[2] = uint32_t(tiles);
+    out_stats[3] = uint32_t(max_cta);
+    out_stats[4] = P.n_ctas();
+  }
+  return 0;
+}
