@@ -270,7 +270,6 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 2);
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
   const PoolGeom& g = a.g;
   const uint32_t S = g.S;
   if (threadIdx.x == 0) ATTN_TR(5, 0);
@@ -301,6 +300,10 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: everything above overlapped the previous
+  // kernel (the projection GEMM that writes Q and appends this layer's K/V)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
   if (threadIdx.x == 0) ATTN_TR(5, 1);
 
   if (warp == 0 || warp == 3) {
@@ -691,8 +694,18 @@ static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, c
     cudaFuncSetAttribute(attn_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
     set = true;
   }
-  if (a.trace) attn_tc_kernel<D, true><<<a.n_items, 384, TcCfg<D>::SMEM, s>>>(pool_map, q_map, a);
-  else attn_tc_kernel<D, false><<<a.n_items, 384, TcCfg<D>::SMEM, s>>>(pool_map, q_map, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.n_items);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = TcCfg<D>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: prologue overlaps the GEMM's tail
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (a.trace) cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, true>, pool_map, q_map, a);
+  else cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, false>, pool_map, q_map, a);
 }
 
 void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {

@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
+  // every CTA of this grid is resident: let the next kernel (attention, launched
+  // with programmatic serialization) start its prologue on SMs as they free up
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < nk; ++kb) {
