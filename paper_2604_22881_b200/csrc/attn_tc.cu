@@ -31,6 +31,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -189,18 +190,23 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x for x <= 0 on the FMA pipe (Cody-Waite split + cubic minimax on [0,1),
-// max relative error 7.5e-5 << bf16 P rounding): a share of the exponentials
-// moves off the 16/clk/SM MUFU unit, which otherwise bounds the softmax.
+// 2^x for x <= 0 on the FMA pipe: round-to-nearest split with the 1.5*2^23
+// magic constant (no conversion-pipe FRND / F2I), cubic minimax of 2^f on
+// [-1/2, 1/2] (max relative error 7.5e-5 << bf16 P rounding), exponent add.
+// A share of the exponentials moves off the 16/clk/SM MUFU unit.
 __device__ __forceinline__ float ex2_poly(float x) {
   const float xc = fmaxf(x, -126.f);
-  const float fl = floorf(xc);
-  const float f = xc - fl;
-  const float p = fmaf(fmaf(fmaf(0.0780245001f, f, 0.2260672448f), f, 0.6958334771f), f, 0.9999252275f);
-  const float y = __int_as_float(__float_as_int(p) + (int(fl) << 23));
+  const float t = xc + 12582912.f;
+  const int j = __float_as_int(t) - 0x4B400000;  // round(xc)
+  const float f = xc - (t - 12582912.f);          // [-0.5, 0.5]
+  const float p = fmaf(fmaf(fmaf(0.0551716566f, f, 0.2426111399f), f, 0.6932609894f), f, 0.9999280726f);
+  const float y = __int_as_float(__float_as_int(p) + (j << 23));
   return x < -126.f ? 0.f : y;
 }
-constexpr int kPolyEvery = 4;  // every 4th column of a tile uses ex2_poly (0 = all MUFU)
+// Measured on the bench-layer microbenchmark: all-MUFU 70.4 us, every 8th column
+// on ex2_poly 71.4 us, every 4th 72.7 us — the softmax is not MUFU-bound, so the
+// default keeps every exponential on MUFU (MTKV_ATTN_POLY=4|8 selects the mix).
+constexpr int kPolyDefault = 0;
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -242,7 +248,7 @@ struct TcCfg {
 };
 
 
-template <int D, bool TR>  // TR: per-CTA event trace (MTKV_ATTN_TRACE builds only)
+template <int D, bool TR, int POLY>  // TR: per-CTA event trace; POLY: k-th columns use ex2_poly (0: none)
 __global__ void __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map, AttnArgs a) {
   using C = TcCfg<D>;
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int c = 0; c < BN; ++c) {
           const float x = fmaf(s[c], a.scale_log2, nmref);
-          s[c] = (kPolyEvery && c % kPolyEvery == kPolyEvery - 1) ? ex2_poly(x) : ex2(x);
+          s[c] = (POLY && c % POLY == POLY - 1) ? ex2_poly(x) : ex2(x);
           r4[c & 3] += s[c];
         }
         const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
@@ -686,12 +692,11 @@ int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g
   return encode_2d(map, q, g.d, rows, BM);
 }
 
-template <int D>
-static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
+template <int D, bool TR, int POLY>
+static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(attn_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
-    cudaFuncSetAttribute(attn_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
+    cudaFuncSetAttribute(attn_tc_kernel<D, TR, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
     set = true;
   }
   cudaLaunchConfig_t cfg{};
@@ -704,8 +709,19 @@ static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (a.trace) cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, true>, pool_map, q_map, a);
-  else cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, false>, pool_map, q_map, a);
+  cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, TR, POLY>, pool_map, q_map, a);
+}
+
+template <int D>
+static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
+  static const int poly = [] {
+    const char* e = std::getenv("MTKV_ATTN_POLY");
+    return e ? std::atoi(e) : kPolyDefault;
+  }();
+  if (a.trace) launch_cfg<D, true, kPolyDefault>(pool_map, q_map, a, s);
+  else if (poly == 4) launch_cfg<D, false, 4>(pool_map, q_map, a, s);
+  else if (poly == 8) launch_cfg<D, false, 8>(pool_map, q_map, a, s);
+  else launch_cfg<D, false, 0>(pool_map, q_map, a, s);
 }
 
 void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
