@@ -1,15 +1,15 @@
 // Host-side planning of one batch's attention work (both attention kernels).
 //
 // tcgen05 path: every (request, head, 128-row query tile) segment needs the
-// 64-key tiles of its visible logical key space (incremental attention of the
+// 128-key tiles of its visible logical key space (incremental attention of the
 // fresh rows over the cached prefix + themselves, reference model.cpp:104).
 // Per head, the concatenation of the segments' tiles is cut into contiguous,
 // equal-length ranges, one per persistent CTA (sibling CTAs of the H heads run
 // aligned ranges), so every SM streams the same number of K/V bytes regardless
 // of how history lengths are distributed over the batch; a range that crosses a
 // segment boundary becomes several pieces.
-// Each piece yields two partial slots (one per softmax pipeline); the combine
-// in gate_norm_kernel merges a segment's slots.
+// Each piece yields one partial slot; the combine in gate_norm_kernel merges a
+// segment's slots.
 //
 // mma.sync path (head_dim < 64): one CTA per (request, head, query tile, key
 // split of split_keys positions), one slot per split.
@@ -117,14 +117,11 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
     for (const AttnPiece& pc : P.pieces) ++npc[pc.seg];
     for (uint32_t sg = 0; sg < P.segs.size(); ++sg) {
       P.segs[sg].part_base = P.n_slots;
-      P.segs[sg].n_parts = 2 * npc[sg];
-      P.n_slots += 2 * npc[sg];
+      P.segs[sg].n_parts = npc[sg];
+      P.n_slots += npc[sg];
     }
     std::vector<uint32_t> used(P.segs.size(), 0);
-    for (AttnPiece& pc : P.pieces) {
-      pc.part = P.segs[pc.seg].part_base + used[pc.seg];
-      used[pc.seg] += 2;
-    }
+    for (AttnPiece& pc : P.pieces) pc.part = P.segs[pc.seg].part_base + used[pc.seg]++;
     return;
   }
   // mma.sync path: 64/128-row query tiles over positions, 512-key splits for
@@ -188,7 +185,7 @@ extern "C" int mtkv_attention_plan_check(uint32_t n, const uint32_t* n_hist, con
         const AttnPiece& pc = P.pieces[i];
         if (pc.seg >= P.segs.size() || pc.lo >= pc.hi || pc.hi > P.segs[pc.seg].n_tiles) return 2;
         const AttnSeg& sg = P.segs[pc.seg];
-        if (pc.part < sg.part_base || pc.part + 2 > sg.part_base + sg.n_parts) return 3;
+        if (pc.part < sg.part_base || pc.part + 1 > sg.part_base + sg.n_parts) return 3;
         for (uint32_t x = pc.lo; x < pc.hi; ++x) ++cover[pc.seg][x];
         t += pc.hi - pc.lo;
       }

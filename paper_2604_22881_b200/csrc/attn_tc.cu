@@ -1,7 +1,7 @@
 // Incremental prefix-reuse attention on the 5th-gen tensor cores (sm_100a).
 //
 // Persistent kernel: one CTA per SM streams a contiguous, equal-length range
-// of 64-key tiles (attn_plan.cpp); the range is a list of pieces, each a key
+// of 128-key tiles (attn_plan.cpp); the range is a list of pieces, each a key
 // range of one (request, head, 128-row query tile) segment. The K/V rings keep
 // streaming across piece boundaries, so an SM never idles on a prologue.
 // Warp roles (384 threads):
@@ -9,16 +9,22 @@
 //               straight out of the paged pool (no gather pass), NK-stage ring
 //   warp 3      V producer: same for V, NV-stage ring (V stays until PV, K is
 //               released as soon as S = Q K^T has completed)
-//   warp 1      MMA issuer (one elected lane): tcgen05.cp of the piece's Q into
-//               TMEM, S = Q K^T (A = Q in TMEM, B = K in smem) and O += P V
-//               (A = P in TMEM, B = V in smem) with tcgen05.mma kind::f16
+//   warp 1      MMA issuer (one elected lane of a uniform warp): tcgen05.cp of
+//               the piece's Q into TMEM, S = Q K^T (A = Q in TMEM, B = K in
+//               smem) into one of two S buffers, O += P V (A = P in TMEM over
+//               its S buffer, B = V in smem) with tcgen05.mma kind::f16
 //   warp 2      TMEM allocator, then Q loader (TMA, double-buffered per piece; a
 //               buffer is refilled once its Q is in TMEM and the piece's
 //               epilogue, which stages O through it, is done)
-//   warps 4..11 two softmax pipelines (tiles of a piece alternate between
-//               them): thread r owns query row r (= TMEM lane r): tcgen05.ld of
-//               its S row, mask, online softmax in base 2, P -> TMEM (bf16x2,
-//               tcgen05.st), lazy O rescale, epilogue O/l + lse per piece
+//   warps 4..11 softmax: thread r of warpgroup w owns query row r (= TMEM lane
+//               r) and key columns [64w, 64w + 64) of each tile: tcgen05.ld of
+//               its S half, mask, row max exchanged with the other warpgroup
+//               through shared memory, online softmax in base 2, P -> TMEM
+//               (bf16x2, tcgen05.st over the S buffer), lazy O rescale of its
+//               half of O; per piece an epilogue O/l + lse
+// While the softmax warps turn S(t) into P(t), the tensor core computes S(t+1)
+// into the other buffer; S(t+2) is issued right behind PV(t), which in the
+// in-order tensor pipe has read P(t) from the buffer S(t+2) overwrites.
 // Logical key space: the user's keys [0, KA) padded to a page boundary, then
 // the request's candidate keys (their own scratch pages), so every page-sized
 // slice of a tile is one TMA box. Keys past the end load as zeros (TMA OOB).
@@ -26,7 +32,7 @@
 // Shared-memory operand layouts (canonical UMMA, 128-byte swizzle):
 //   Q, K : K-major  [rows][64-elem blocks], SBO = 1024 B, +32 B per K=16 step
 //   V    : MN-major [keys][64-dim blocks],  SBO = 1024 B, LBO = one block
-// TMEM columns per pipeline: S (64 fp32) | P (32 x bf16x2) | O (D fp32); then Q (D/2).
+// TMEM columns: S/P buffers (2 x 128 fp32) | O (D fp32) | Q (D/2).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -40,7 +46,7 @@ namespace mtkv_b200 {
 namespace tc {
 
 constexpr int BM = 128;   // query rows per tile (TMEM lanes)
-constexpr int BN = 64;    // keys per tile
+constexpr int BN = 128;   // keys per tile (two warpgroups x 64 columns)
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -234,19 +240,22 @@ struct TcCfg {
   static constexpr int NB = D / 64;                      // 64-element column blocks of Q/K/V
   static constexpr uint32_t QBLK = BM * 128;             // 128 rows x 128 B
   static constexpr uint32_t Q_BYTES = NB * QBLK;
-  static constexpr uint32_t KBLK = BN * 128;             // 64 keys x 128 B
+  static constexpr uint32_t KBLK = BN * 128;             // BN keys x 128 B
   static constexpr uint32_t T_BYTES = NB * KBLK;         // one K (or V) tile
-  static constexpr int NK = D == 128 ? 5 : 8;            // K ring stages
-  static constexpr int NV = D == 128 ? 5 : 8;            // V ring stages
-  static constexpr uint32_t S_COL = 0, P_COL = BN, O_COL = BN + BN / 2, PIPE = BN + BN / 2 + D;
-  static constexpr uint32_t Q_COL = 2 * PIPE;            // Q (bf16x2) after the two pipelines
+#ifndef MTKV_ATTN_NK
+#define MTKV_ATTN_NK 3
+#endif
+  static constexpr int NK = D == 128 ? MTKV_ATTN_NK : 4;      // K ring stages (128-key tiles)
+  static constexpr int NV = D == 128 ? 5 - MTKV_ATTN_NK : 4;  // V ring stages (V is held until PV)
+  // TMEM: two S buffers (fp32, BN cols; P(t) is written as bf16x2 over the first
+  // BN/2 columns of S(t)'s buffer), O (D cols), Q (D/2 cols)
+  static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, Q_COL = 2 * BN + D;
   static constexpr uint32_t TMEM_COLS = Q_COL + D / 2 <= 256 ? 256 : 512;
   static_assert(Q_COL + D / 2 <= 512, "TMEM budget");
-  static constexpr size_t SMEM = 1024 + 2 * Q_BYTES + size_t(NK + NV) * T_BYTES + 256;
-  static_assert(8 * 32 * (D / 4) * 4 <= Q_BYTES, "epilogue staging fits one Q buffer");
+  static constexpr size_t SMEM = 2 * Q_BYTES + size_t(NK + NV) * T_BYTES + 2 * 2 * BM * 4 + 256;
   static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(8 * 32 * (D / 4) * 4 <= Q_BYTES, "epilogue staging fits one Q buffer");
 };
-
 
 template <int D, bool TR, int POLY>  // TR: per-CTA event trace; POLY: k-th columns use ex2_poly (0: none)
 __global__ void __launch_bounds__(384, 1)
@@ -254,25 +263,26 @@ __global__ void __launch_bounds__(384, 1)
   using C = TcCfg<D>;
   constexpr int NB = C::NB, NK = C::NK, NV = C::NV;
   constexpr uint32_t QBLK = C::QBLK, KBLK = C::KBLK, T_BYTES = C::T_BYTES, Q_BYTES = C::Q_BYTES;
-  constexpr float kRescale = 8.f;  // lazy rescale threshold (log2 units): p <= 2^8 between rescales
+  constexpr int HC = BN / 2;        // key columns per softmax warpgroup
+  constexpr float kRescale = 8.f;   // lazy rescale threshold (log2 units): p <= 2^8 between rescales
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];  // 128-B swizzled tiles need 1024-B alignment
+  uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;                          // [2] Q buffers (TMA target -> TMEM; then epilogue staging)
   uint8_t* sK = sQ + 2 * Q_BYTES;              // [NK] K tiles
   uint8_t* sV = sK + NK * T_BYTES;             // [NV] V tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NV * T_BYTES);
+  float* sMax = reinterpret_cast<float*>(sV + NV * T_BYTES);  // [2 tiles][2 warpgroups][BM] row-max exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sMax + 2 * 2 * BM);
   uint64_t* full_k = bars;
   uint64_t* empty_k = full_k + NK;
   uint64_t* full_v = empty_k + NK;
   uint64_t* empty_v = full_v + NV;
-  uint64_t* s_full = empty_v + NV;  // [2 pipes] S tile in TMEM
-  uint64_t* s_free = s_full + 2;    // [2] S read by softmax
-  uint64_t* p_full = s_free + 2;    // [2] P in TMEM (+ O rescaled)
-  uint64_t* o_done = p_full + 2;    // [2] PV completed
-  uint64_t* q_full = o_done + 2;    // [2] Q buffer landed
+  uint64_t* s_full = empty_v + NV;  // [2] S buffer computed
+  uint64_t* p_full = s_full + 2;    // P(t) in TMEM + O rescaled (8 softmax warps)
+  uint64_t* o_done = p_full + 1;    // PV(t) completed
+  uint64_t* q_full = o_done + 1;    // [2] Q buffer landed
   uint64_t* q_empty = q_full + 2;   // [2] Q buffer copied into TMEM
-  uint64_t* epi_done = q_empty + 2; // [2] both pipelines' epilogues (staged in that Q buffer) done
+  uint64_t* epi_done = q_empty + 2; // [2] the piece's epilogue (staged in that Q buffer) done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 2);
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -281,20 +291,19 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) ATTN_TR(5, 0);
 
   if (threadIdx.x == 0) {
-    // a stage is released by the 4 warps of the softmax pipeline that owns the
-    // tile: K once they have loaded S (so S, hence the K read, completed), V once
-    // they have seen that tile's PV complete (keeps commits off the MMA thread)
-    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 4); }
-    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 4); }
-    for (int p = 0; p < 2; ++p) {
-      mbar_init(&s_full[p], 1);
-      mbar_init(&s_free[p], 4);
-      mbar_init(&p_full[p], 4);
-      mbar_init(&o_done[p], 1);
-      mbar_init(&q_full[p], 1);
-      mbar_init(&q_empty[p], 1);
-      mbar_init(&epi_done[p], 8);
+    // a K stage is released by the 8 softmax warps once they hold S (so the S
+    // MMA, hence its K read, completed); a V stage once they saw that tile's PV
+    // complete — keeps commits off the MMA issuer
+    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 8); }
+    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 8); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1);
+      mbar_init(&epi_done[b], 8);
     }
+    mbar_init(p_full, 8);
+    mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* ring = isv ? sV : sK;
     const uint32_t NS = isv ? NV : NK;
     const uint32_t ppt = BN / S;  // pages per tile
-    uint32_t gt = 0;
+    uint32_t gt = 0, st = 0, ph = 0;
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const AttnSeg sg = a.segs[P.seg];
@@ -339,13 +348,12 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t cache_t0 = P.lo;
       int rows_cache = row_of(uint64_t(P.lo) * ppt + lane);  // 32 consecutive pages per refresh
       for (uint32_t t = P.lo; t < P.hi; ++t, ++gt) {
-        const uint32_t st = gt % NS;
         if ((t - cache_t0) * ppt >= 32) {
           cache_t0 = t;
           rows_cache = row_of(uint64_t(t) * ppt + lane);
         }
         if (lane == 0) {
-          if (gt >= NS) mbar_wait(&empty[st], ((gt / NS) - 1) & 1);
+          if (gt >= NS) mbar_wait(&empty[st], ph ^ 1);
           if (!isv) ATTN_TR(0, gt);
           mbar_expect_tx(&full[st], T_BYTES);
         }
@@ -360,6 +368,7 @@ __global__ void __launch_bounds__(384, 1)
               tma_load_2d(dst + b * KBLK + i * S * 128, &pool_map, int(col + 64 * b), row, &full[st]);
           }
         }
+        if (++st == NS) { st = 0; ph ^= 1; }
       }
     }
   } else if (warp == 2) {
@@ -383,35 +392,27 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: S(g+2) is issued before PV(g) ----------------
-    // Tiles alternate between the two softmax pipelines; S of a pipeline's next
-    // tile only needs that pipeline to have loaded the previous S into registers,
-    // so it executes while the pipeline is still computing P. (Issuing S and PV
-    // from two different warps measured slower: 88 vs 65 us per launch.) The
-    // whole warp runs branch-free uniform code: stage / phase counters advance
-    // incrementally and one elected lane issues through predicated instructions.
+    // ---------------- MMA issuer ----------------
+    // Order: S(0), S(1), then per tile t: PV(t) (waits for P(t)), S(t+2) into
+    // S(t)'s buffer — in order behind PV(t), which has read P(t) from it. S(t+1)
+    // runs on the tensor core while the softmax warps turn S(t) into P(t).
+    // The whole warp runs branch-free uniform code; one elected lane issues.
     if (pe > pb) {
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
           (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       const uint64_t dq0 = sdesc(s32(sQ), 16, 1024), dk0 = sdesc(s32(sK), 16, 1024), dv0 = sdesc(s32(sV), KBLK, 1024);
       const bool leader = elect_one();
-      // S cursor: piece, tiles left in it, tile-in-piece, pieces seen, K stage/phase, S tiles per pipeline
-      uint32_t s_pc = pb, s_left = 0, s_j = 0, s_k = 0, stk = 0, phk = 0, s_cnt0 = 0, s_cnt1 = 0, s_g = 0;
-      // PV cursor
-      uint32_t v_pc = pb, v_left = 0, v_j = 0, stv = 0, phv = 0, pph = 0 /* bit p: phase of p_full[p] */, v_g = 0;
       uint32_t total = 0;
       for (uint32_t pc = pb; pc < pe; ++pc) total += a.pieces[pc].hi - a.pieces[pc].lo;
-      {
-        const AttnPiece P0 = a.pieces[pb];
-        s_left = v_left = P0.hi - P0.lo;
-      }
+      // S cursor
+      uint32_t s_pc = pb, s_left = a.pieces[pb].hi - a.pieces[pb].lo, s_k = 0, s_j = 0, stk = 0, phk = 0, s_g = 0;
       auto issue_s = [&]() {
-        const uint32_t p = s_j & 1;
+        const uint32_t b = s_g & 1;
         ATTN_TR(9, s_g);
         if (s_j == 0) {
-          // new piece: copy its Q into TMEM, in order with the previous piece's
-          // S MMAs that still read the old Q
+          // new piece: copy its Q into TMEM, in order behind the previous
+          // piece's S MMAs that still read the old Q
           const uint32_t qb = s_k & 1;
           mbar_wait(&q_full[qb], (s_k >> 1) & 1);
           tc_after();
@@ -421,20 +422,16 @@ __global__ void __launch_bounds__(384, 1)
             tmem_cp_if(leader, tmem + C::Q_COL + kk * 8, aq + ((((kk / 4) * QBLK + (kk % 4) * 32)) >> 4));
           mma_commit_if(leader, &q_empty[qb]);  // smem Q buffer reusable once copied
         }
-        const uint32_t cnt = p ? s_cnt1 : s_cnt0;  // S tiles this pipeline already got
-        if (cnt > 0) mbar_wait(&s_free[p], (cnt - 1) & 1);
         mbar_wait(&full_k[stk], phk);
         tc_after();
         const uint64_t bk = dk0 + ((stk * T_BYTES) >> 4);
-        const uint32_t d_tmem = tmem + p * C::PIPE + C::S_COL;
+        const uint32_t d_tmem = tmem + C::S_COL + b * BN;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_ts_if(leader, d_tmem, tmem + C::Q_COL + kk * 8, bk + (((kk / 4) * KBLK + (kk % 4) * 32) >> 4), idesc_s,
                     kk > 0);
-        mma_commit_if(leader, &s_full[p]);
+        mma_commit_if(leader, &s_full[b]);
         if (leader) ATTN_TR(1, s_g);
-        // advance
-        if (p) ++s_cnt1; else ++s_cnt0;
         if (++stk == NK) { stk = 0; phk ^= 1; }
         ++s_g;
         ++s_j;
@@ -445,53 +442,48 @@ __global__ void __launch_bounds__(384, 1)
           if (s_pc < pe) { const AttnPiece Pn = a.pieces[s_pc]; s_left = Pn.hi - Pn.lo; }
         }
       };
-      for (uint32_t g = 0; g < total; ++g) {
-        // keep S up to two tiles ahead of PV; the first S of a new piece waits for
-        // that piece's Q and must not hold back the previous piece's last PVs
-        while (s_g < total && s_g < g + 3) {
-          if (s_j == 0 && s_g > g && !mbar_ready(&q_full[s_k & 1], (s_k >> 1) & 1)) break;
-          issue_s();
-        }
-        const uint32_t p = v_j & 1;
-        ATTN_TR(10, v_g);
-        mbar_wait(&p_full[p], (pph >> p) & 1);
+      issue_s();
+      if (s_g < total) issue_s();
+      uint32_t v_pc = pb, v_left = a.pieces[pb].hi - a.pieces[pb].lo, v_j = 0, stv = 0, phv = 0;
+      for (uint32_t gg = 0; gg < total; ++gg) {
+        ATTN_TR(10, gg);
+        mbar_wait(p_full, gg & 1);
         mbar_wait(&full_v[stv], phv);
         tc_after();
         const uint64_t bv = dv0 + ((stv * T_BYTES) >> 4);
-        const uint32_t d_tmem = tmem + p * C::PIPE + C::O_COL, a_tmem = tmem + p * C::PIPE + C::P_COL;
+        const uint32_t a_tmem = tmem + C::S_COL + (gg & 1) * BN;  // P(gg) over S(gg)'s buffer
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
-          mma_ts_if(leader, d_tmem, a_tmem + kk * 8, bv + ((kk * 2048) >> 4), idesc_o, (v_j >= 2 || kk > 0) ? 1u : 0u);
-        mma_commit_if(leader, &o_done[p]);
-        if (leader) ATTN_TR(2, v_g);
-        pph ^= 1u << p;
+          mma_ts_if(leader, tmem + C::O_COL, a_tmem + kk * 8, bv + ((kk * 2048) >> 4), idesc_o,
+                    (v_j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_if(leader, o_done);
+        if (leader) ATTN_TR(2, gg);
         if (++stv == NV) { stv = 0; phv ^= 1; }
-        ++v_g;
         ++v_j;
         if (--v_left == 0) {
           ++v_pc;
           v_j = 0;
           if (v_pc < pe) { const AttnPiece Pn = a.pieces[v_pc]; v_left = Pn.hi - Pn.lo; }
         }
+        if (s_g < total) issue_s();
       }
     }
   } else if (warp >= 4) {
-    // ---------------- softmax pipelines ----------------
-    const uint32_t p = (warp - 4) / 4;             // pipeline
+    // ---------------- softmax: 8 warps, warpgroup w takes key columns [w*BN/2, (w+1)*BN/2) ----------------
+    const uint32_t wg = (warp - 4) / 4;            // column half
     const uint32_t r = (threadIdx.x - 128) % 128;  // query row == TMEM lane
     const uint32_t lane_base = (32u * (warp % 4)) << 16;
-    const uint32_t s_col = tmem + lane_base + p * C::PIPE + C::S_COL;
-    const uint32_t p_col = tmem + lane_base + p * C::PIPE + C::P_COL;
-    const uint32_t o_col = tmem + lane_base + p * C::PIPE + C::O_COL;
-    uint32_t u = 0;          // tiles this pipeline has processed (barrier phases)
-    uint32_t gbase = 0;      // CTA-wide index of the current piece's first tile
-    int32_t pend_v = -1;     // tile whose V stage this pipeline still has to release
+    const uint32_t o_col = tmem + lane_base + C::O_COL + wg * (D / 2);
+    uint32_t t_all = 0;      // tiles processed (barrier phases)
+    int32_t pend_v = -1;     // tile whose V stage this warp still has to release
+    uint32_t stk = 0;        // K stage of the current tile
     auto release_v = [&]() {
       if (pend_v >= 0) {
         if (lane == 0) mbar_arrive(&empty_v[uint32_t(pend_v) % NV]);
         pend_v = -1;
       }
     };
+    auto named_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const AttnSeg sg = a.segs[P.seg];
@@ -507,113 +499,115 @@ __global__ void __launch_bounds__(384, 1)
       // valid keys of this row: user keys [0, u_end), candidate keys [KAp, c_end)
       const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
       const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
-      // the same bounds relative to the piece's first key, clamped to [0, span] (32-bit per tile)
-      const uint64_t kb0 = uint64_t(P.lo) * BN;
+      // the same bounds relative to this warpgroup's first key of the piece, clamped (32-bit per tile)
+      const uint64_t kb0 = uint64_t(P.lo) * BN + wg * HC;
       const int64_t span = int64_t(P.hi - P.lo) * BN;
-      auto rel = [&](uint64_t x) { return int(min(max(int64_t(x) - int64_t(kb0), int64_t(0)), span)); };
+      auto rel = [&](uint64_t x) { return int(min(max(int64_t(x) - int64_t(kb0), int64_t(-1)), span)); };
       const int ue = rel(u_end), cl = rel(KAp), ce = rel(c_end);
-      float m_ref = -INFINITY, l_run = 0.f;
-      uint32_t mine = 0;
-      for (uint32_t t = P.lo + p; t < P.hi; t += 2, ++u, ++mine) {
-        mbar_wait(&s_full[p], u & 1);
+      float m_ref = -INFINITY, l_part = 0.f;
+      for (uint32_t t = P.lo; t < P.hi; ++t, ++t_all) {
+        const uint32_t b = t_all & 1;
+        mbar_wait(&s_full[b], (t_all >> 1) & 1);
         tc_after();
-        if (threadIdx.x % 128 == 0) ATTN_TR(3, u * 2 + p);
-        float s[BN];
+        if (threadIdx.x % 128 == 0) ATTN_TR(3, t_all);
+        float s[HC];
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) tmem_ld32(s_col + c * 32, s + c * 32);
+        for (int c = 0; c < HC / 32; ++c) tmem_ld32(tmem + lane_base + C::S_COL + b * BN + wg * HC + c * 32, s + c * 32);
         tmem_wait_ld();
-        if (threadIdx.x % 128 == 0) ATTN_TR(6, u * 2 + p);
         tc_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&s_free[p]);
-          mbar_arrive(&empty_k[(gbase + t - P.lo) % NK]);
-        }
+        if (lane == 0) mbar_arrive(&empty_k[stk]);
+        if (++stk == NK) stk = 0;
         const int kb = int(t - P.lo) * BN;
-        const int cu = min(max(ue - kb, 0), BN), c_lo = min(max(cl - kb, 0), BN), c_hi = min(max(ce - kb, 0), BN);
-        if (cu != BN) {
+        const int cu = min(max(ue - kb, 0), HC), c_lo = min(max(cl - kb, 0), HC), c_hi = min(max(ce - kb, 0), HC);
+        if (cu != HC) {
 #pragma unroll
-          for (int c = 0; c < BN; ++c) {
+          for (int c = 0; c < HC; ++c) {
             const bool ok = c < cu || (c >= c_lo && c < c_hi);
             s[c] = ok ? s[c] : -INFINITY;
           }
         }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < BN; ++c) m4[c & 3] = fmaxf(m4[c & 3], s[c]);
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * a.scale_log2;
+        for (int c = 0; c < HC; ++c) m4[c & 3] = fmaxf(m4[c & 3], s[c]);
+        // row max over both halves: exchange through shared memory (double-buffered by tile)
+        float* mx_buf = sMax + b * 2 * BM;
+        mx_buf[wg * BM + r] = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        named_sync();  // also orders both halves' S loads before either writes P over them
+        const float mx = fmaxf(mx_buf[r], mx_buf[BM + r]) * a.scale_log2;
+        if (threadIdx.x % 128 == 0) ATTN_TR(6, t_all);
         float alpha = 1.f;
-        if (mx > m_ref + kRescale) {  // lazy rescale: p <= 2^8 between rescales
+        if (mx > m_ref + kRescale) {
           alpha = m_ref == -INFINITY ? 0.f : ex2(m_ref - mx);
           m_ref = mx;
         }
         const float nmref = m_ref == -INFINITY ? 0.f : -m_ref;
         float r4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < BN; ++c) {
+        for (int c = 0; c < HC; ++c) {
           const float x = fmaf(s[c], a.scale_log2, nmref);
           s[c] = (POLY && c % POLY == POLY - 1) ? ex2_poly(x) : ex2(x);
           r4[c & 3] += s[c];
         }
-        const float rs = (r4[0] + r4[1]) + (r4[2] + r4[3]);
-        l_run = l_run * alpha + rs;
-        if (threadIdx.x % 128 == 0) ATTN_TR(7, u * 2 + p);
-        if (u > 0) {  // this pipeline's previous PV must finish before P / O are touched
-          mbar_wait(&o_done[p], (u - 1) & 1);
+        l_part = l_part * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
+        if (threadIdx.x % 128 == 0) ATTN_TR(7, t_all);
+        // P over the first BN/2 columns of this S buffer (this half's HC/2 columns)
+#pragma unroll
+        for (int hlf = 0; hlf < HC / 32; ++hlf) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = pack2(s[hlf * 32 + 2 * c], s[hlf * 32 + 2 * c + 1]);
+          tmem_st16(tmem + lane_base + C::S_COL + b * BN + wg * (HC / 2) + hlf * 16, pk);
+        }
+        if (t != P.lo) {  // the previous PV must finish before O is rescaled
+          mbar_wait(o_done, (t_all - 1) & 1);
           tc_after();
           release_v();
-        }
-        if (threadIdx.x % 128 == 0) ATTN_TR(8, u * 2 + p);
-        // P -> TMEM in two halves (keeps the live register set small), then the lazy O rescale
-#pragma unroll
-        for (int hlf = 0; hlf < 2; ++hlf) {
-          uint32_t pk[BN / 4];
-#pragma unroll
-          for (int c = 0; c < BN / 4; ++c) pk[c] = pack2(s[hlf * (BN / 2) + 2 * c], s[hlf * (BN / 2) + 2 * c + 1]);
-          tmem_st16(p_col + hlf * (BN / 4), pk);
-        }
-        if (mine > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            float o[32];
-            tmem_ld32(o_col + c * 32, o);
-            tmem_wait_ld();
+            for (int c = 0; c < D / 64; ++c) {
+              float o[32];
+              tmem_ld32(o_col + c * 32, o);
+              tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st32(o_col + c * 32, o);
+              for (int i = 0; i < 32; ++i) o[i] *= alpha;
+              tmem_st32(o_col + c * 32, o);
+            }
           }
         }
+        if (threadIdx.x % 128 == 0) ATTN_TR(8, t_all);
         tmem_wait_st();
         tc_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[p]);
-        pend_v = int32_t(gbase + t - P.lo);
-        if (threadIdx.x % 128 == 0) ATTN_TR(4, u * 2 + p);
-        if (threadIdx.x % 128 == 96) ATTN_TR(11, u * 2 + p);
+        if (lane == 0) mbar_arrive(p_full);
+        pend_v = int32_t(t_all);
+        if (threadIdx.x % 128 == 0) ATTN_TR(4, t_all);
       }
-      // epilogue: this pipeline's O / l and lse (base 2) into slot part + p
+      // ---- epilogue: O / l and lse (base 2) into slot `part` ----
       if (threadIdx.x == 128) ATTN_TR(5, 3 + 2 * (pc - pb));
       const uint32_t qi = q0 + r;
-      if (mine > 0) {
-        mbar_wait(&o_done[p], (u - 1) & 1);
-        tc_after();
-        release_v();
-      }
+      mbar_wait(o_done, (t_all - 1) & 1);
+      tc_after();
+      release_v();
+      float* l_buf = sMax + (t_all & 1) * 2 * BM;  // the buffer the next tile's max exchange will use
+      l_buf[wg * BM + r] = l_part;
+      named_sync();
+      const float l_run = l_buf[r] + l_buf[BM + r];
+      named_sync();  // both halves read l before the buffer is reused
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      const size_t prow = size_t(P.part + p) * BM + r;
-      if (mine > 0) {
+      {
         // O/l -> HBM through a per-warp staging tile in this piece's (already
         // copied) Q buffer: tcgen05.ld gives one row per thread, the staged
         // tile is written back as whole 128-B row segments (coalesced)
-        constexpr int CW = D / 4;                 // staged columns per pass
-        constexpr int C4 = CW / 4;                // float4 chunks per staged row
+        constexpr int CW = D / 4;                 // staged columns per pass (8 warps x 32 rows x CW fp32 = Q_BYTES)
+        constexpr int C4 = CW / 4;
         const uint32_t kq = pc - pb, qb = kq & 1;
         mbar_wait(&q_empty[qb], (kq >> 1) & 1);   // tcgen05.cp of this Q buffer finished
         float* stg = reinterpret_cast<float*>(sQ + qb * Q_BYTES) + (warp - 4) * 32 * CW;
         const uint32_t row0 = (warp % 4) * 32;    // first TMEM lane (query row) of this warp
-        float* dst_slot = a.part_o + size_t(P.part + p) * BM * D;
+        float* dst_slot = a.part_o + size_t(P.part) * BM * D + wg * (D / 2);
 #pragma unroll 1
-        for (int c = 0; c < D / CW; ++c) {
+        for (int c = 0; c < D / 2 / CW; ++c) {
           float o[32];
           if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
           else tmem_ld16(o_col + c * CW, o);
@@ -633,12 +627,12 @@ __global__ void __launch_bounds__(384, 1)
           __syncwarp();
         }
       }
-      if (qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
-      gbase += P.hi - P.lo;
+      const size_t prow = size_t(P.part) * BM + r;
+      if (wg == 0 && qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
       if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
       tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
     }
     if (threadIdx.x == 128) ATTN_TR(5, 2);
   }

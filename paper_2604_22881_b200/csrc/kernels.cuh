@@ -44,11 +44,11 @@ struct ReqDev {
 // gate_norm_kernel merges a segment's slots.
 struct AttnSeg {
   uint32_t req, head, qtile;
-  uint32_t n_tiles;     // tcgen05 path: 64-key tiles visible to the query tile
+  uint32_t n_tiles;     // tcgen05 path: 128-key tiles visible to the query tile
   uint32_t part_base, n_parts;
 };
 // tcgen05 path: a piece = key tiles [lo, hi) of one segment, run by one CTA of
-// the persistent kernel; slot `part` (pipeline 0) and `part + 1` (pipeline 1).
+// the persistent kernel; its partial result goes to slot `part`.
 struct AttnPiece {
   uint32_t seg, lo, hi, part;
 };
@@ -167,7 +167,7 @@ struct AttnPlan {
   uint32_t n_slots = 0;
   uint32_t n_ctas() const { return cta_off.empty() ? 0 : uint32_t(cta_off.size() - 1); }
 };
-constexpr uint32_t kTcBM = 128, kTcBN = 64;
+constexpr uint32_t kTcBM = 128, kTcBN = 128;
 // Fills reqs[r].seg0/qtiles (and split_keys for the mma path) and the plan.
 // tcgen05: balanced contiguous key-tile ranges over `ctas` persistent CTAs.
 void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& plan);

@@ -8,7 +8,7 @@ import sys
 import numpy as np
 C, K, T = 64, 12, 96
 a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(C, K, T).astype(np.int64)
-names = ["Kiss", "S", "PV", "s_rdy", "P0", "", "ld", "exp", "odone", "Swt", "PVwt", "P3"]
+names = ["Kiss", "S", "PV", "s_rdy", "Pdone", "", "mx", "exp", "orsc", "Swt", "PVwt", "P3"]
 order = [0, 9, 1, 3, 6, 7, 8, 4, 11, 10, 2]
 for c in range(min(int(sys.argv[2]) if len(sys.argv) > 2 else 3, C)):
     t0 = a[c, 5, 0]
