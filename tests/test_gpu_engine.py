@@ -217,6 +217,34 @@ def test_model_dims_of_bench_config():
     assert worst <= LOGIT_TOL
 
 
+def test_model_dims_of_gr8_config():
+    """d = 512 (H=4, D=128; configs[3] width): 8 k-blocks through the 2-stage
+    tcgen05 GEMM ring, N=2048 projection, 16-column gate/norm lanes."""
+    kv = dict(num_layers=2, num_heads=4, head_dim=128, page_size=32, chunk_size=64, device_pages=64,
+              offload_quota=256)
+    mc = dict(num_layers=2, num_heads=4, head_dim=128, vocab=128, seed=5)
+    rng = np.random.default_rng(1)
+    trace = []
+    for t in range(9):
+        u = t % 3
+        dn = int(rng.integers(20, 150))
+        trace.append({"ts": t, "user": u, "dn": dn, "nc": 4, "tokens": rng.integers(0, 128, dn).tolist(),
+                      "cands": rng.integers(0, 128, 4).tolist()})
+    eng = mtkv.Engine(_kv(kv), mode="hierarchical", backend="value", batch_size=3,
+                      model=mtkv.ModelConfig(**mc), keep_logits=True)
+    from oracle.oracle import Oracle
+    o = Oracle(kv, mode="hierarchical", batch_size=3, model=ModelParams(**mc))
+    worst = 0.0
+    for b in batches(trace, 3):
+        eng.process_batch(b)
+        o.process_batch(b)
+        assert eng.plans() == o.plans()
+        for g, r in zip(eng.last_logits(), o.logits()):
+            worst = max(worst, _rel_logit_err(g, r))
+    print("d=512 worst rel logit err", worst)
+    assert worst <= LOGIT_TOL
+
+
 def _paged_pool(L, P, S, d, seed=0):
     g = torch.Generator(device="cuda").manual_seed(seed)
     return (torch.randn(L, P, 2, S, d, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
