@@ -212,11 +212,13 @@ def run_b200(args, cfg):
     prefill, revisits = make_workload(cfg, warm + 3 * K, rank, world)
     # pinned host store sized for the run up front (no cudaHostAlloc while serving)
     tok_bytes = kv.token_kv_bytes()
-    host_mb = int(1.3 * (cfg["users"] * (cfg["history"] + 2 * kv.chunk_size) + len(revisits) * cfg["delta"])
-                  * tok_bytes / 2**20) + 1024
+    # one pinned extent per user sized to its persisted prefix over the run, so a
+    # user's onload is a single large copy-engine transfer (host-link peak)
+    extent_mb = -(-((cfg["history"] + 16 * cfg["delta"]) * tok_bytes) // 2**20)
+    host_mb = int(1.1 * cfg["users"] * extent_mb) + 1024
     ppu = -(-(cfg["history"] + 16 * cfg["delta"]) // cfg["page"])
     eng = mtkv.Engine(kv, cost, mode="hierarchical", backend="value", batch_size=B, model=model,
-                      device=local, host_reserve_mb=host_mb, planner=args.planner,
+                      device=local, host_reserve_mb=host_mb, host_extent_mb=extent_mb, planner=args.planner,
                       max_users=cfg["users"] + 64, max_user_pages=2 * ppu + 64)
     # ---- warm-up: prefill histories (untimed), then the first revisit batches ----
     pb = max(1, 65536 // cfg["history"])

@@ -116,6 +116,9 @@ typedef struct {
   uint32_t device_planner;   /* 1: user lookup, LRU update, victim selection and page allocation
                                 (manager.cpp:74 prepare_metadata) run on the GPU over device tables */
   uint32_t max_users;        /* device planner: user-table capacity (0 = 65536) */
+  uint32_t host_extent_mb;   /* pinned host tier: per-user extent size (0 = 8 MB); an onload is one
+                                copy-engine transfer per extent, so extents sized to a user's
+                                persisted prefix keep the host link at its large-copy peak */
 } mtkv_engine_options;
 
 /* ---- configuration (core.cpp) ---- */
@@ -238,7 +241,8 @@ int mtkv_op_paged_attention(float* out, const void* q, const void* pool, const u
  * its p_pre[r] cached keys and themselves; its page ids start at
  * d_pages[page_off[r]] (host arrays page_off / n_q / p_pre). repeat > 1 launches
  * the attention kernel `repeat` times and returns the mean device ms of launches
- * 2..repeat in *ms_per_launch (kernel benchmarking); out gets the merged result. */
+ * 2..repeat in *ms_per_launch, each timed alone after an L2-evicting memset
+ * (kernel benchmarking); out gets the merged result. */
 int mtkv_op_paged_attention_batch(float* out, const void* q, const void* pool, const uint32_t* d_pages,
                                   const uint32_t* page_off, const uint32_t* n_q, const uint64_t* p_pre,
                                   uint32_t n_req, uint32_t layer, const mtkv_kv_config* kv, uint32_t num_pages,

@@ -107,7 +107,7 @@ class _EngineOpts(C.Structure):
                 ("seed", C.c_uint64), ("model", _ModelCfg), ("device", C.c_int),
                 ("max_batch_tokens", C.c_uint32), ("max_user_pages", C.c_uint32),
                 ("keep_logits", C.c_uint32), ("profile", C.c_uint32), ("host_reserve_mb", C.c_uint64),
-                ("device_planner", C.c_uint32), ("max_users", C.c_uint32)]
+                ("device_planner", C.c_uint32), ("max_users", C.c_uint32), ("host_extent_mb", C.c_uint32)]
 
 
 class _GenCfg(C.Structure):
@@ -488,7 +488,7 @@ class Engine(_ManagerView):
                  backend: str = "tag", batch_size: int = 1, model: ModelConfig | None = None,
                  device: int = 0, keep_logits: bool = False, profile: bool = False, seed: int = 1,
                  host_reserve_mb: int = 0, planner: str = "host", max_users: int = 0,
-                 max_user_pages: int = 0):
+                 max_user_pages: int = 0, host_extent_mb: int = 0):
         self.kv, self.mode, self.backend, self.batch_size = kv, mode, backend, batch_size
         self.model = model
         if backend == "value" and model is None:
@@ -503,6 +503,7 @@ class Engine(_ManagerView):
             raise Error("planner must be 'host' or 'device'")
         o.device_planner = int(planner == "device")
         o.max_users, o.max_user_pages = int(max_users), int(max_user_pages)
+        o.host_extent_mb = int(host_extent_mb)
         self._h = lib().mtkv_engine_create(C.byref(kv._c()), C.byref((cost or CostModel())._c()),
                                            C.byref(o))
         if not self._h:

@@ -202,7 +202,8 @@ int Engine::init(std::string& err) {
     off_slot_batch_.assign(slots, -1);
   }
   // host extents of ~8 MB (>= 1 chunk) and slabs of >= 4 extents
-  chunks_per_extent_ = uint32_t(std::max<size_t>(1, (size_t(8) << 20) / chunk_bytes_));
+  const size_t extent_bytes = size_t(opt_.host_extent_mb ? opt_.host_extent_mb : 8) << 20;
+  chunks_per_extent_ = uint32_t(std::max<size_t>(1, extent_bytes / chunk_bytes_));
   slab_bytes_ = std::max<size_t>(size_t(64) << 20, chunk_bytes_ * chunks_per_extent_ * 4);
   if (opt_.mode == MTKV_MODE_HIERARCHICAL) {
     // reserve the expected host store now: cudaHostAlloc takes the driver lock

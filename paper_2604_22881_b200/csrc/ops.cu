@@ -169,24 +169,36 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
       cudaMemsetAsync(trace, 0, trace_bytes, s);
       a.trace = trace;
     }
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    // repeat > 1: launch 0 is the warm-up; launches 1..repeat-1 are timed one by
+    // one with CUDA events, each after a 256 MB memset that evicts L2 (so a
+    // launch never reuses K/V the previous launch left in the 126 MB L2)
+    std::vector<cudaEvent_t> ev;
+    void* flush = nullptr;
     if (repeat > 1 && ms_per_launch) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
+      ev.resize(2 * (repeat - 1));
+      for (auto& x : ev) cudaEventCreate(&x);
+      cudaMallocAsync(&flush, size_t(256) << 20, s);
     }
     for (uint32_t it = 0; it < std::max<uint32_t>(repeat, 1); ++it) {
-      if (it == 1 && e0) cudaEventRecord(e0, s);  // first launch is the warm-up
+      if (it >= 1 && !ev.empty()) {
+        cudaMemsetAsync(flush, int(it & 0xFF), size_t(256) << 20, s);
+        cudaEventRecord(ev[2 * (it - 1)], s);
+      }
       if (tc) launch_attention_tc(pmap, qmap, a, s);
       else launch_attention(a, s);
+      if (it >= 1 && !ev.empty()) cudaEventRecord(ev[2 * (it - 1) + 1], s);
     }
-    if (e0) {
-      cudaEventRecord(e1, s);
-      cudaEventSynchronize(e1);
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
-      *ms_per_launch = ms / float(repeat - 1);
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
+    if (!ev.empty()) {
+      cudaStreamSynchronize(s);
+      double tot = 0;
+      for (uint32_t it = 1; it < repeat; ++it) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[2 * (it - 1)], ev[2 * (it - 1) + 1]);
+        tot += ms;
+      }
+      *ms_per_launch = float(tot / double(repeat - 1));
+      for (auto& x : ev) cudaEventDestroy(x);
+      cudaFreeAsync(flush, s);
     }
     if (trace) {
       std::vector<unsigned long long> h(trace_bytes / 8);

@@ -4,8 +4,9 @@
 page 32; fresh rows per request = 64 new + 8 candidates, plus the lost tail
 (0..127 rows) for the ~69 % of requests that were onloaded from the host tier
 (the bench's steady-state mix). Pages are a random permutation of a 40 K-page pool
-(no locality). Times `repeat` back-to-back launches with CUDA events and reports
-algorithmic GB/s against MEASURED_PEAKS.json (same accounting as bench.py).
+(no locality). Times `repeat` launches one by one with CUDA events, each after
+a 256 MB memset that evicts L2, and reports algorithmic GB/s against
+MEASURED_PEAKS.json (same accounting as bench.py).
 
   python tools/attn_bench.py [--repeat 50] [--seed 0] [--tag name]
 """

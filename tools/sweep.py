@@ -36,10 +36,10 @@ def run_mode(cfg: dict, mode: str, steps: int, warm: int, pool_frac: float | Non
     B = cfg["batch"]
     prefill, revisits = bench.make_workload(cfg, warm + steps, 0, 1)
     tok = kv.token_kv_bytes()
-    host_mb = int(1.3 * (cfg["users"] * (cfg["history"] + 2 * kv.chunk_size) + len(revisits) * cfg["delta"])
-                  * tok / 2**20) + 1024 if mode == "hierarchical" else 0
+    extent_mb = -(-((cfg["history"] + 16 * cfg["delta"]) * tok) // 2**20)
+    host_mb = int(1.1 * cfg["users"] * extent_mb) + 1024 if mode == "hierarchical" else 0
     eng = mtkv.Engine(kv, mtkv.CostModel(bus_bandwidth=55e9), mode=mode, backend="value", batch_size=B,
-                      model=model, host_reserve_mb=host_mb)
+                      model=model, host_reserve_mb=host_mb, host_extent_mb=extent_mb)
     if mode != "recompute":  # recompute keeps no cache: the first visit is not a prefill
         pb = max(1, 65536 // cfg["history"])
         for i in range(0, len(prefill), pb):
