@@ -46,6 +46,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "requests/sec & tokens/sec at fixed hit ratio, p99 latency, 1/2/4/8 B200 vs CPU"
+# MTKV_BENCH_ONE_GPU=1: all torchrun ranks on GPU 0 (functional check of the sharded
+# multi-rank flow on a one-GPU box; its throughput is not a scaling number)
+ONE_GPU = os.environ.get("MTKV_BENCH_ONE_GPU") == "1"
 H2D_PEAK_GBS = 55.5  # measured pinned H2D, 64-256 MiB copies (profiles/r01_probe_h2d.json)
 
 CONFIGS = {
@@ -201,7 +204,12 @@ def run_b200(args, cfg):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ONE_GPU:  # functional check of the N>1 path on a one-GPU box: ranks share GPU 0, gloo reductions
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if ONE_GPU:
+        local = 0
     torch.cuda.set_device(local)
     kv = kv_config(cfg)
     cost = mtkv.CostModel(bus_bandwidth=55e9)  # measured pinned H2D on the B200 box (probe)
@@ -309,9 +317,10 @@ def run_b200(args, cfg):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     n_req, fresh_tokens = K * B, phase_a["fresh_tokens"]
     if dist:
-        t = torch.tensor([elapsed, e2e_s], dtype=torch.float64, device="cuda")
+        rdev = "cpu" if ONE_GPU else "cuda"
+        t = torch.tensor([elapsed, e2e_s], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        c = torch.tensor([n_req, fresh_tokens], dtype=torch.float64, device="cuda")
+        c = torch.tensor([n_req, fresh_tokens], dtype=torch.float64, device=rdev)
         dist.all_reduce(c, op=dist.ReduceOp.SUM)
         elapsed, e2e_s = t.tolist()
         n_all, tok_all = c.tolist()

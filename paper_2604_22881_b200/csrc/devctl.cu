@@ -55,7 +55,7 @@ struct Smem {
   uint64_t red64[kThreads / 32];
   uint32_t red32[kThreads / 32];
   uint64_t prefix, need, wtotal;
-  uint32_t prefix_bits, n_vict, fail, fail_at, i_end, fail_kind;
+  uint32_t prefix_bits, n_vict, fail, fail_at, i_end, n_ids, n_ev, top;
   uint64_t vkey[kMaxVictims];   // (stamp) of each victim
   uint32_t vslot[kMaxVictims];
   uint32_t vnp[kMaxVictims];    // pages a victim frees
@@ -383,11 +383,11 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     sm.max_pos = hi;
     sm.final_top = top;
     sm.scratch_total = sm.fail == CTL_OK ? scr : 0;
-    sm.red32[0] = ids;
-    sm.red32[1] = vi;  // evictions
+    sm.n_ids = ids;
+    sm.n_ev = vi;  // evictions
   }
   __syncthreads();
-  const uint32_t i_end = sm.i_end, n_ev = sm.red32[1], n_ids = sm.red32[0];
+  const uint32_t i_end = sm.i_end, n_ev = sm.n_ev, n_ids = sm.n_ids;
   // value at stack position x as seen by request i's pops: the latest victim push
   // (victims are ordered in time) covering x among those evicted up to request i,
   // else the stack's content before the batch
