@@ -315,9 +315,11 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
-  // programmatic dependent launch: everything above overlapped the previous
-  // kernel (the projection GEMM that writes Q and appends this layer's K/V)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // Programmatic dependent launch: this grid may start while the projection
+  // GEMM that writes Q and appends this layer's fresh K/V is still running.
+  // Everything before it in the stream (batch metadata, the cached prefix in the
+  // pool, the previous consumer of part_o) is complete, so only reads of Q and
+  // of tiles holding fresh keys wait for the GEMM (griddepcontrol.wait below).
   const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
   if (threadIdx.x == 0) ATTN_TR(5, 1);
 
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t NS = isv ? NV : NK;
     const uint32_t ppt = BN / S;  // pages per tile
     uint32_t gt = 0, st = 0, ph = 0;
+    bool dep_done = false;        // griddepcontrol.wait executed
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const AttnSeg sg = a.segs[P.seg];
@@ -352,6 +355,10 @@ __global__ void __launch_bounds__(384, 1)
           cache_t0 = t;
           rows_cache = row_of(uint64_t(t) * ppt + lane);
         }
+        if (!dep_done && uint64_t(t + 1) * BN > R.start) {  // tile holds keys this layer's GEMM appends
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          dep_done = true;
+        }
         if (lane == 0) {
           if (gt >= NS) mbar_wait(&empty[st], ph ^ 1);
           if (!isv) ATTN_TR(0, gt);
@@ -373,6 +380,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 2) {
     // ---------------- Q loader: one TMA box per 64-column block, double-buffered ----------------
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // Q is written by the projection GEMM
     if (lane == 0) {
       uint32_t k = 0;
       for (uint32_t pc = pb; pc < pe; ++pc, ++k) {

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--tag", default="")
     ap.add_argument("--requests", type=int, default=64)
+    ap.add_argument("--prefix", type=int, default=4096, help="cached prefix length (keys) before the revisit spread")
     ap.add_argument("--tail-frac", type=float, default=0.69,
                     help="fraction of requests carrying a recomputed tail (0..127 extra fresh rows)")
     args = ap.parse_args()
@@ -36,7 +37,7 @@ def main():
     L, H, D, S = 4, 2, 128, 32
     d = H * D
     n = args.requests
-    p_pre = (4096 + 64 * rng.integers(0, 16, n)).astype(np.uint64)
+    p_pre = (args.prefix + 64 * rng.integers(0, 16, n)).astype(np.uint64)
     tail = np.where(rng.random(n) < args.tail_frac, rng.integers(0, 128, n), 0)
     n_q = (72 + tail).astype(np.uint32)
     pages_per = ((p_pre + n_q + S - 1) // S).astype(np.int64)
