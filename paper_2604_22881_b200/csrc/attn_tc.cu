@@ -597,20 +597,23 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(o_done, (t_all - 1) & 1);
       tc_after();
       release_v();
+      if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb));
       float* l_buf = sMax + (t_all & 1) * 2 * BM;  // the buffer the next tile's max exchange will use
       l_buf[wg * BM + r] = l_part;
       named_sync();
       const float l_run = l_buf[r] + l_buf[BM + r];
       named_sync();  // both halves read l before the buffer is reused
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb) + 1);
       {
         // O/l -> HBM through a per-warp staging tile in this piece's (already
         // copied) Q buffer: tcgen05.ld gives one row per thread, the staged
         // tile is written back as whole 128-B row segments (coalesced)
         constexpr int CW = D / 4;                 // staged columns per pass (8 warps x 32 rows x CW fp32 = Q_BYTES)
         constexpr int C4 = CW / 4;
-        const uint32_t kq = pc - pb, qb = kq & 1;
-        mbar_wait(&q_empty[qb], (kq >> 1) & 1);   // tcgen05.cp of this Q buffer finished
+        // the tcgen05.cp that read this Q buffer completed before this piece's first
+        // S (the s_full commits track all earlier tcgen05 operations)
+        const uint32_t qb = (pc - pb) & 1;
         float* stg = reinterpret_cast<float*>(sQ + qb * Q_BYTES) + (warp - 4) * 32 * CW;
         const uint32_t row0 = (warp % 4) * 32;    // first TMEM lane (query row) of this warp
         float* dst_slot = a.part_o + size_t(P.part) * BM * D + wg * (D / 2);
@@ -633,6 +636,7 @@ __global__ void __launch_bounds__(384, 1)
               *reinterpret_cast<float4*>(dst_slot + size_t(row0 + rr) * D + c * CW + 4 * k) = v;
           }
           __syncwarp();
+          if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb) + 2 + c);
         }
       }
       const size_t prow = size_t(P.part) * BM + r;

@@ -39,3 +39,13 @@ for c in range(min(int(sys.argv[2]) if len(sys.argv) > 2 else 3, C)):
     n = int((a[c, 0] > 0).sum())
     print(f"CTA {c}: tiles traced {n}, last S {(a[c,1,n-1]-t0)/1e3:.2f}us, end {(a[c,5,2]-t0)/1e3:.2f}us, "
           f"epilogues " + ", ".join(f"#{k}: {s:.2f}-{e:.2f}" for k, s, e in ep))
+# epilogue phases (kind 11, slots 4k..4k+3): o_done passed, l exchanged, store pass 1, store pass 2
+for c in range(min(int(sys.argv[2]) if len(sys.argv) > 2 else 3, C)):
+    t0 = a[c, 5, 0]
+    for k in range(8):
+        if not a[c, 5, 3 + 2 * k]:
+            continue
+        st = (a[c, 5, 3 + 2 * k] - t0) / 1e3
+        ph = [(a[c, 11, 4 * k + i] - t0) / 1e3 if a[c, 11, 4 * k + i] else float("nan") for i in range(4)]
+        print(f"CTA {c} epilogue #{k}: start {st:.2f} odone {ph[0]:.2f} l {ph[1]:.2f} pass1 {ph[2]:.2f} pass2 {ph[3]:.2f} "
+              f"end {(a[c, 5, 4 + 2 * k] - t0) / 1e3:.2f}")
