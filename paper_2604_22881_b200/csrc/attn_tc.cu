@@ -86,6 +86,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(s32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -259,7 +268,8 @@ struct TcCfg {
 
 template <int D, bool TR, int POLY>  // TR: per-CTA event trace; POLY: k-th columns use ex2_poly (0: none)
 __global__ void __launch_bounds__(384, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map, AttnArgs a) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map,
+                   const __grid_constant__ CUtensorMap part_map, AttnArgs a) {
   using C = TcCfg<D>;
   constexpr int NB = C::NB, NK = C::NK, NV = C::NV;
   constexpr uint32_t QBLK = C::QBLK, KBLK = C::KBLK, T_BYTES = C::T_BYTES, Q_BYTES = C::Q_BYTES;
@@ -492,6 +502,16 @@ __global__ void __launch_bounds__(384, 1)
       }
     };
     auto named_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    int32_t epi_pending = -1;  // piece whose staged partial tiles may still be read by TMA stores
+    auto flush_epi = [&]() {   // hand the staging (Q) buffer back once the stores have read it
+      if (epi_pending >= 0) {
+        if (lane == 0) {
+          bulk_wait_read<0>();
+          mbar_arrive(&epi_done[uint32_t(epi_pending) & 1]);
+        }
+        epi_pending = -1;
+      }
+    };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const AttnSeg sg = a.segs[P.seg];
@@ -589,6 +609,7 @@ __global__ void __launch_bounds__(384, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
         pend_v = int32_t(t_all);
+        flush_epi();
         if (threadIdx.x % 128 == 0) ATTN_TR(4, t_all);
       }
       // ---- epilogue: O / l and lse (base 2) into slot `part` ----
@@ -616,27 +637,56 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t qb = (pc - pb) & 1;
         float* stg = reinterpret_cast<float*>(sQ + qb * Q_BYTES) + (warp - 4) * 32 * CW;
         const uint32_t row0 = (warp % 4) * 32;    // first TMEM lane (query row) of this warp
-        float* dst_slot = a.part_o + size_t(P.part) * BM * D + wg * (D / 2);
+        if constexpr (CW == 32) {
+          // D = 128: the warp's 64 O columns leave in four 32-row x 16-column fp32
+          // tiles through TMA bulk tensor stores, alternating between two 2 KB
+          // halves of its staging area, so no pass waits on HBM writes; rows past
+          // the query tile's valid rows land in unused rows of the slot
+          constexpr int PW = 16;  // columns per pass
 #pragma unroll 1
-        for (int c = 0; c < D / 2 / CW; ++c) {
-          float o[32];
-          if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
-          else tmem_ld16(o_col + c * CW, o);
-          tmem_wait_ld();
+          for (int c = 0; c < D / 2 / PW; ++c) {
+            float* half = stg + (c & 1) * 32 * PW;
+            if (c >= 2) {
+              if (lane == 0) bulk_wait_read<1>();  // the store that used this half has read it
+              __syncwarp();
+            }
+            float o[16];
+            tmem_ld16(o_col + c * PW, o);
+            tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < C4; ++k)
-            *reinterpret_cast<float4*>(stg + lane * CW + ((k ^ (lane % C4)) << 2)) =
-                make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
-          __syncwarp();
-#pragma unroll
-          for (int it = 0; it < C4; ++it) {
-            const uint32_t qd = lane + 32 * it, rr = qd / C4, k = qd % C4;
-            const float4 v = *reinterpret_cast<const float4*>(stg + rr * CW + ((k ^ (rr % C4)) << 2));
-            if (q0 + row0 + rr < q_end)
-              *reinterpret_cast<float4*>(dst_slot + size_t(row0 + rr) * D + c * CW + 4 * k) = v;
+            for (int k = 0; k < PW / 4; ++k)
+              *reinterpret_cast<float4*>(half + lane * PW + 4 * k) =
+                  make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&part_map, half, int(wg * (D / 2) + c * PW), int(P.part * BM + row0));
+              bulk_commit();
+            }
+            if (threadIdx.x == 128 && c < 2) ATTN_TR(11, 4 * (pc - pb) + 2 + c);
           }
-          __syncwarp();
-          if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb) + 2 + c);
+          epi_pending = int32_t(pc - pb);  // epi_done is signalled once the stores have read the staging
+        } else {
+          float* dst_slot = a.part_o + size_t(P.part) * BM * D + wg * (D / 2);
+#pragma unroll 1
+          for (int c = 0; c < D / 2 / CW; ++c) {
+            float o[32];
+            tmem_ld16(o_col + c * CW, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < C4; ++k)
+              *reinterpret_cast<float4*>(stg + lane * CW + ((k ^ (lane % C4)) << 2)) =
+                  make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < C4; ++it) {
+              const uint32_t qd = lane + 32 * it, rr = qd / C4, k = qd % C4;
+              const float4 v = *reinterpret_cast<const float4*>(stg + rr * CW + ((k ^ (rr % C4)) << 2));
+              if (q0 + row0 + rr < q_end)
+                *reinterpret_cast<float4*>(dst_slot + size_t(row0 + rr) * D + c * CW + 4 * k) = v;
+            }
+            __syncwarp();
+          }
         }
       }
       const size_t prow = size_t(P.part) * BM + r;
@@ -644,9 +694,11 @@ __global__ void __launch_bounds__(384, 1)
       if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
+      if (epi_pending < 0 && lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
     }
     if (threadIdx.x == 128) ATTN_TR(5, 2);
+    flush_epi();
+    if (lane == 0) bulk_wait_all();  // the partial tiles are in global memory before the CTA retires
   }
   tc_before();
   __syncthreads();
@@ -693,13 +745,29 @@ int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
   return encode_2d(map, pool, g.d, uint64_t(g.L) * g.num_pages * 2 * g.S, g.S);
 }
 
+// partial O slots [slots * 128 rows][D] fp32, box = 16 cols x 32 rows, no swizzle
+// (the attention epilogue's staged tiles; D = 128)
+int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t D) {
+  const cuuint64_t dims[2] = {D, rows};
+  const cuuint64_t strides[1] = {cuuint64_t(D) * 4};
+  const cuuint32_t box[2] = {16, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(part_o), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 // fresh-row queries [rows][d], box = 64 cols x 128 rows (rows past the buffer load as zeros)
 int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g) {
   return encode_2d(map, q, g.d, rows, BM);
 }
 
 template <int D, bool TR, int POLY>
-static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
+static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+                       const AttnArgs& a, cudaStream_t s) {
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_tc_kernel<D, TR, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
@@ -715,25 +783,27 @@ static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, co
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, TR, POLY>, pool_map, q_map, a);
+  cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, TR, POLY>, pool_map, q_map, part_map, a);
 }
 
 template <int D>
-static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
+static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+                        const AttnArgs& a, cudaStream_t s) {
   static const int poly = [] {
     const char* e = std::getenv("MTKV_ATTN_POLY");
     return e ? std::atoi(e) : kPolyDefault;
   }();
-  if (a.trace) launch_cfg<D, true, kPolyDefault>(pool_map, q_map, a, s);
-  else if (poly == 4) launch_cfg<D, false, 4>(pool_map, q_map, a, s);
-  else if (poly == 8) launch_cfg<D, false, 8>(pool_map, q_map, a, s);
-  else launch_cfg<D, false, 0>(pool_map, q_map, a, s);
+  if (a.trace) launch_cfg<D, true, kPolyDefault>(pool_map, q_map, part_map, a, s);
+  else if (poly == 4) launch_cfg<D, false, 4>(pool_map, q_map, part_map, a, s);
+  else if (poly == 8) launch_cfg<D, false, 8>(pool_map, q_map, part_map, a, s);
+  else launch_cfg<D, false, 0>(pool_map, q_map, part_map, a, s);
 }
 
-void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s) {
+void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+                         const AttnArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
-  if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, a, s);
-  else launch_tc_d<128>(pool_map, q_map, a, s);
+  if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, part_map, a, s);
+  else launch_tc_d<128>(pool_map, q_map, part_map, a, s);
 }
 
 }  // namespace mtkv_b200

@@ -660,7 +660,15 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
           q_map_ptr_ = q_.p;
           q_map_bytes_ = q_.bytes;
         }
-        launch_attention_tc(pool_map_, q_map_, aa, comp_);
+        if (part_map_ptr_ != part_o_.p || part_map_bytes_ != part_o_.bytes) {
+          if (make_part_map(&part_map_, part_o_.p, part_o_.bytes / (size_t(g_.D) * sizeof(float)), g_.D)) {
+            err = "engine: cuTensorMapEncodeTiled (attention partials) failed";
+            return MTKV_ERROR;
+          }
+          part_map_ptr_ = part_o_.p;
+          part_map_bytes_ = part_o_.bytes;
+        }
+        launch_attention_tc(pool_map_, q_map_, part_map_, aa, comp_);
       } else {
         launch_attention(aa, comp_);
       }

@@ -115,6 +115,9 @@ class Engine {
   uint32_t pool_map_pages_ = 0;
   const void* q_map_ptr_ = nullptr;
   size_t q_map_bytes_ = 0;
+  alignas(64) CUtensorMap part_map_{};
+  const void* part_map_ptr_ = nullptr;
+  size_t part_map_bytes_ = 0;
 
   // pinned host memory: slabs -> per-user extents -> chunks
   static constexpr size_t kSpareSlabs = 2;

@@ -151,7 +151,9 @@ namespace mtkv_b200 {
 bool attn_tc_supported(const PoolGeom& g);
 int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g);
 int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g);
-void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s);
+int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t D);
+void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+                         const AttnArgs& a, cudaStream_t s);
 int num_sms();
 }  // namespace mtkv_b200
 

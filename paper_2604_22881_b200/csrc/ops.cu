@@ -155,8 +155,9 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
   a.bq = plan.bm;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
   if (e == cudaSuccess) {
-    alignas(64) CUtensorMap pmap, qmap;
-    if (tc && (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, rows, g))) {
+    alignas(64) CUtensorMap pmap, qmap, omap;
+    if (tc && (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, rows, g) ||
+               make_part_map(&omap, a.part_o, uint64_t(plan.n_slots) * plan.bm, g.D))) {
       cudaFreeAsync(buf, s);
       set_last_error("paged_attention: cuTensorMapEncodeTiled failed");
       return MTKV_ERROR;
@@ -184,7 +185,7 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
         cudaMemsetAsync(flush, int(it & 0xFF), size_t(256) << 20, s);
         cudaEventRecord(ev[2 * (it - 1)], s);
       }
-      if (tc) launch_attention_tc(pmap, qmap, a, s);
+      if (tc) launch_attention_tc(pmap, qmap, omap, a, s);
       else launch_attention(a, s);
       if (it >= 1 && !ev.empty()) cudaEventRecord(ev[2 * (it - 1) + 1], s);
     }
