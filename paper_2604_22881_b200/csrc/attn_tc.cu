@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(384, 1)
           cache_t0 = t;
           rows_cache = row_of(uint64_t(t) * ppt + lane);
         }
-        if (!dep_done && uint64_t(t + 1) * BN > R.start) {  // tile holds keys this layer's GEMM appends
+        if (!dep_done && uint64_t(t + 1) * BN > R.dep_start) {  // tile holds keys this layer's GEMM appends
           asm volatile("griddepcontrol.wait;" ::: "memory");
           dep_done = true;
         }

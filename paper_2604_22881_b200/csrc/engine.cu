@@ -415,6 +415,12 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     x.scratch_off = recompute_ ? t_soff[r] : R.scratch_off;
     x.n_scratch = recompute_ ? t_ns[r] : R.n_scratch;
     x.user = R.plan.user;
+    x.dep_start = x.start;
+    for (uint32_t q = 0; q < r; ++q)  // an earlier occurrence of the user appends keys this one reads
+      if (w.reqs[q].slot == R.slot) {
+        x.dep_start = rd[q].dep_start;
+        break;
+      }
     rows += x.n_q;
     ncand_total += x.n_cand;
     max_hist = std::max(max_hist, x.n_hist);

@@ -35,6 +35,8 @@ struct ReqDev {
   uint32_t qtiles;      // query tiles of `bm` rows per head
   uint32_t split_keys;  // mma.sync path: keys per split
   uint32_t user;
+  uint64_t dep_start;   // keys >= dep_start may be appended by this batch's projection GEMM
+                        // (the user's first occurrence in the batch; later occurrences read them)
 };
 
 // Attention work decomposition. A segment = (request, head, query tile of bm

@@ -101,6 +101,7 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
     x.q_row0 = rows;
     x.n_q = x.n_hist = n_q[r];
     x.start = p_pre[r];
+    x.dep_start = p_pre[r];
     x.pages_off = page_off[r];
     x.n_pages = uint32_t((p_pre[r] + n_q[r] + g.S - 1) / g.S);
     rows += n_q[r];
