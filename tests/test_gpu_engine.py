@@ -217,6 +217,36 @@ def test_model_dims_of_bench_config():
     assert worst <= LOGIT_TOL
 
 
+def test_repeated_user_within_batch():
+    """A user appearing twice in one batch: the second occurrence attends over the
+    keys the first one appends in the same projection GEMM (guards the early,
+    pre-griddepcontrol.wait K/V loads of the PDL-launched attention)."""
+    kv = dict(num_layers=2, num_heads=2, head_dim=128, page_size=16, chunk_size=32, device_pages=400,
+              offload_quota=256)
+    mc = dict(num_layers=2, num_heads=2, head_dim=128, vocab=64, seed=9)
+    rng = np.random.default_rng(4)
+    trace = []
+    for t in range(24):
+        u = [0, 1, 0, 2, 1, 1][t % 6]
+        dn = int(rng.integers(30, 200))
+        trace.append({"ts": t, "user": u, "dn": dn, "nc": 3, "tokens": rng.integers(0, 64, dn).tolist(),
+                      "cands": rng.integers(0, 64, 3).tolist()})
+    from oracle.oracle import Oracle
+    for rep in range(3):
+        eng = mtkv.Engine(_kv(kv), mode="hierarchical", backend="value", batch_size=6,
+                          model=mtkv.ModelConfig(**mc), keep_logits=True)
+        o = Oracle(kv, mode="hierarchical", batch_size=6, model=ModelParams(**mc))
+        worst = 0.0
+        for b in batches(trace, 6):
+            eng.process_batch(b)
+            o.process_batch(b)
+            assert eng.plans() == o.plans()
+            for g, r in zip(eng.last_logits(), o.logits()):
+                worst = max(worst, _rel_logit_err(g, r))
+        print(f"repeated users rep {rep}: worst rel logit err {worst:.3e}")
+        assert worst <= LOGIT_TOL
+
+
 def test_model_dims_of_gr8_config():
     """d = 512 (H=4, D=128; configs[3] width): 8 k-blocks through the 2-stage
     tcgen05 GEMM ring, N=2048 projection, 16-column gate/norm lanes."""
