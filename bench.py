@@ -267,6 +267,7 @@ def run_b200(args, cfg):
     eng_lat, attn_ms, attn_launches, attn_bytes = [], 0.0, 0, 0
     copy_stat = [0.0, 0, 0.0, 0, 0, 0]  # scatter ms, chunks, gather ms, chunks, launches, launches
     plan_ms, ctl_ms = [], []
+    proj_stat = [0.0, 0, 0]  # projection GEMM ms, launches, rows (summed over launches)
     d = cfg["H"] * cfg["D"]
     rb0 = eng.report()
     k0 = warm + K
@@ -280,6 +281,8 @@ def run_b200(args, cfg):
         pm, km = eng.last_plan_ms()
         plan_ms.append(pm)
         ctl_ms.append(km)
+        pm_, pn_, prow_ = eng.last_proj_ms()
+        proj_stat[0] += pm_; proj_stat[1] += pn_; proj_stat[2] += prow_ * pn_
         sm, sc, gm, gc = eng.last_chunk_copy_ms()
         copy_stat[0] += sm; copy_stat[1] += sc; copy_stat[2] += gm; copy_stat[3] += gc
         copy_stat[4] += 1 if sc else 0; copy_stat[5] += 1 if gc else 0
@@ -396,6 +399,15 @@ def run_b200(args, cfg):
             gbs = 2 * ch * cb / (ms / 1e3) / 1e9
             kern[name] = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                           "launches": nl, "avg_launch_us": ms / nl * 1e3, "bytes_per_launch": 2 * ch * cb / nl}
+    if proj_stat[1]:
+        # projection GEMM + fused paged K/V append: read activations (rows x d) and
+        # W_in (d x 4d), write u | q (rows x 2d) and the K | V append (rows x 2d), bf16
+        d_ = cfg["H"] * cfg["D"]
+        pbytes = proj_stat[2] * d_ * 2 * 5 + proj_stat[1] * d_ * 4 * d_ * 2
+        gbs = pbytes / (proj_stat[0] / 1e3) / 1e9
+        kern["gemm_tc_proj (+ fused paged K/V append)"] = {
+            "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak, "launches": proj_stat[1],
+            "avg_launch_us": proj_stat[0] / proj_stat[1] * 1e3, "bytes_per_launch": pbytes / proj_stat[1]}
     line["roofline"]["other_kernels"] = kern
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, seconds=args.cpu_seconds)

@@ -185,6 +185,9 @@ double mtkv_engine_last_attention_ms(mtkv_engine* e, uint32_t* launches);
 /* profile mode: device ms of the last batch's onload scatter (staging -> pages,
  * store.hpp:89) and offload gather (pages -> offload slots, store.hpp:106), with
  * the chunk counts they moved */
+/* profile mode: device ms of the last batch's projection GEMMs, which append the
+ * fresh rows' K/V into their pages (store.hpp:123 append), with launches and rows */
+double mtkv_engine_last_proj_ms(mtkv_engine* e, uint32_t* launches, uint64_t* rows);
 int mtkv_engine_last_chunk_copy_ms(mtkv_engine* e, double* scatter_ms, uint32_t* scatter_chunks,
                                    double* gather_ms, uint32_t* gather_chunks);
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e);

@@ -129,6 +129,7 @@ EXPORTED_SYMBOLS = [
     "mtkv_engine_last_plan_ms",
     "mtkv_engine_check_conservation", "mtkv_engine_read_user_kv",
     "mtkv_engine_last_batch_ms", "mtkv_engine_last_attention_ms", "mtkv_engine_last_chunk_copy_ms",
+    "mtkv_engine_last_proj_ms",
     "mtkv_engine_kernel_launches",
     "mtkv_engine_set_profile",
     "mtkv_report", "mtkv_last_plans", "mtkv_last_evictions", "mtkv_known_users", "mtkv_user_state",
@@ -180,6 +181,7 @@ def lib():
                                                  C.POINTER(C.c_uint16), u64]),
         "mtkv_engine_last_batch_ms": (C.c_double, [vp]),
         "mtkv_engine_last_attention_ms": (C.c_double, [vp, u32p]),
+        "mtkv_engine_last_proj_ms": (C.c_double, [vp, u32p, C.POINTER(C.c_uint64)]),
         "mtkv_engine_last_chunk_copy_ms": (C.c_int, [vp, C.POINTER(C.c_double), u32p, C.POINTER(C.c_double), u32p]),
         "mtkv_engine_kernel_launches": (u64, [vp]),
         "mtkv_engine_set_profile": (None, [vp, u32]),
@@ -605,6 +607,12 @@ class Engine(_ManagerView):
         a, b = C.c_double(), C.c_double()
         lib().mtkv_engine_last_plan_ms(self._h, C.byref(a), C.byref(b))
         return a.value, b.value
+
+    def last_proj_ms(self):
+        """(ms, launches, rows) of the last batch's projection GEMMs (profile mode)."""
+        n, rows = C.c_uint32(), C.c_uint64()
+        ms = lib().mtkv_engine_last_proj_ms(self._h, C.byref(n), C.byref(rows))
+        return float(ms), int(n.value), int(rows.value)
 
     def last_chunk_copy_ms(self):
         """(scatter_ms, scatter_chunks, gather_ms, gather_chunks) of the last batch (profile mode)."""

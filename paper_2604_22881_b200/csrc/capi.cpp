@@ -261,6 +261,9 @@ int64_t mtkv_engine_read_user_kv(mtkv_engine* e, uint32_t user, uint32_t layer, 
 
 double mtkv_engine_last_batch_ms(mtkv_engine* e) { return e->e.last_batch_ms(); }
 double mtkv_engine_last_attention_ms(mtkv_engine* e, uint32_t* launches) { return e->e.last_attention_ms(launches); }
+double mtkv_engine_last_proj_ms(mtkv_engine* e, uint32_t* launches, uint64_t* rows) {
+  return e->e.last_proj_ms(launches, rows);
+}
 int mtkv_engine_last_chunk_copy_ms(mtkv_engine* e, double* scatter_ms, uint32_t* scatter_chunks, double* gather_ms,
                                    uint32_t* gather_chunks) {
   return e->e.last_chunk_copy_ms(scatter_ms, scatter_chunks, gather_ms, gather_chunks);

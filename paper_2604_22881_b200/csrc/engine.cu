@@ -425,6 +425,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     ncand_total += x.n_cand;
     max_hist = std::max(max_hist, x.n_hist);
   }
+  last_rows_ = rows;
   if (value_) plan_attention(rd.data(), n, g_, tc, tc ? uint32_t(n_sm_) : 0, plan_);
   const uint32_t bq = plan_.bm;
   const uint32_t n_segs = value_ ? uint32_t(plan_.segs.size()) : 0;
@@ -625,8 +626,8 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     launch_embed(X, w_embed_, d_tok, rows, d, comp_);
     ++launches;
     const bool prof = opt_.profile != 0;
-    if (prof && ev_attn_.size() < 2 * g_.L) {
-      while (ev_attn_.size() < 2 * g_.L) {
+    if (prof && ev_attn_.size() < 4 * g_.L) {
+      while (ev_attn_.size() < 4 * g_.L) {  // [0, 2L): attention pairs; [2L, 4L): projection GEMM pairs
         cudaEvent_t e;
         CK(cudaEventCreate(&e));
         ev_attn_.push_back(e);
@@ -637,7 +638,9 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       ga.A = X; ga.B = w_in_ + size_t(l) * d * 4 * d; ga.M = rows; ga.N = 4 * d; ga.K = d;
       ga.epi = Epi::Proj; ga.out_u = U; ga.out_q = Q; ga.pool = pool; ga.kv_off = d_kv;
       ga.layer_base = size_t(l) * g_.num_pages * 2 * S * d; ga.d = d; ga.kv_stride = S * d;
+      if (prof) CK(cudaEventRecord(ev_attn_[2 * g_.L + 2 * l], comp_));
       if (gemm(ga, x_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
+      if (prof) CK(cudaEventRecord(ev_attn_[2 * g_.L + 2 * l + 1], comp_));
       AttnArgs aa{};
       aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.segs = d_segs; aa.items = d_items;
       aa.n_items = n_items; aa.pieces = d_pieces; aa.cta_off = d_ctaoff;
@@ -906,6 +909,22 @@ double Engine::last_attention_ms(uint32_t* n) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ev_attn_[2 * l], ev_attn_[2 * l + 1]);
     tot += ms;
+  }
+  return tot;
+}
+
+double Engine::last_proj_ms(uint32_t* launches, uint64_t* rows) {
+  *launches = 0;
+  *rows = last_rows_;
+  if (last_slot_ < 0 || !opt_.profile || ev_attn_.size() < 4 * g_.L || !value_) return 0;
+  cudaEventSynchronize(ev_done_[last_slot_]);
+  double tot = 0;
+  for (uint32_t l = 0; l < g_.L; ++l) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ev_attn_[2 * g_.L + 2 * l], ev_attn_[2 * g_.L + 2 * l + 1]) == cudaSuccess) {
+      tot += ms;
+      ++*launches;
+    }
   }
   return tot;
 }

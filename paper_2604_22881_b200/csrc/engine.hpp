@@ -64,6 +64,8 @@ class Engine {
   int gemm(const GemmArgs& a, uint64_t a_rows_alloc, std::string& err);
   // profile mode: device time of the last batch's onload scatter and offload gather
   int last_chunk_copy_ms(double* scatter_ms, uint32_t* scatter_chunks, double* gather_ms, uint32_t* gather_chunks);
+  // profile mode: device ms of the last batch's projection GEMMs (with the fused paged K/V append)
+  double last_proj_ms(uint32_t* launches, uint64_t* rows);
   void report(mtkv_run_report& r) const;
   void set_profile(uint32_t on) { opt_.profile = on; }
   uint32_t batch_size() const { return opt_.batch_size ? opt_.batch_size : 1; }
@@ -106,6 +108,7 @@ class Engine {
   int n_sm_ = 1;                 // persistent attention CTAs
   DevCtl ctl_;                   // device control plane (opt_.device_planner)
   double last_plan_ms_ = 0;
+  uint64_t last_rows_ = 0;
   AttnPlan plan_;                // attention plan of the batch being enqueued
   const char* trace_path_ = std::getenv("MTKV_ATTN_TRACE");
   DevBuf trace_;
