@@ -93,7 +93,7 @@ Engine::~Engine() {
     for (int k = 0; k < kRing; ++k) {
       cudaEventDestroy(ev_onload_[k]); cudaEventDestroy(ev_scatter_[k]);
       cudaEventDestroy(ev_gathered_[k]); cudaEventDestroy(ev_d2h_[k]);
-      cudaEventDestroy(ev_done_[k]); cudaEventDestroy(ev_start_[k]);
+      cudaEventDestroy(ev_done_[k]); cudaEventDestroy(ev_start_[k]); cudaEventDestroy(ev_meta_[k]);
     }
     for (auto e : ev_attn_) cudaEventDestroy(e);
     for (auto e : ev_copy_)
@@ -183,6 +183,7 @@ int Engine::init(std::string& err) {
     CK(cudaEventCreateWithFlags(&ev_d2h_[k], cudaEventDisableTiming));
     CK(cudaEventCreate(&ev_done_[k]));
     CK(cudaEventCreate(&ev_start_[k]));
+    CK(cudaEventCreateWithFlags(&ev_meta_[k], cudaEventDisableTiming));
   }
   if (!recompute_) {
     if (pool_.ensure(size_t(g_.L) * g_.num_pages * 2 * g_.S * g_.d * sizeof(__nv_bfloat16))) {
@@ -369,7 +370,11 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   }
   if (w.rc || n == 0) return MTKV_OK;
   const int k = int(batch_no_ % kRing);
-  if (batch_no_ >= kRing) CK(cudaEventSynchronize(ev_done_[k]));  // ring slot free
+  if (batch_no_ >= kRing) {  // ring slot free: the batch leaving it is complete, its offload D2H included
+    CK(cudaEventSynchronize(ev_done_[k]));
+    if (d2h_rec_batch_[k] >= 0) CK(cudaEventSynchronize(ev_d2h_[k]));
+    d2h_done_upto_ = int64_t(batch_no_) - kRing;
+  }
 
   const uint32_t S = g_.S, d = g_.d, H = g_.H, V = value_ ? opt_.model.vocab : 0;
 
@@ -532,6 +537,14 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     h_chunks[n_on + j] = ChunkWork{off_slots[j], w.offloads[j].pages_off};
   }
 
+  // ---- batch metadata: on the h2d stream, ahead of this batch's chunk copies.
+  // (Issued on comp it shares the H2D copy engine's queue with the chunk copies
+  // and, waiting for comp to reach it, held the next batch's onload back until
+  // this batch's scatter had run: measured ~200 us copy-engine idle per batch.)
+  CK(cudaMemcpyAsync(db, hb, off, cudaMemcpyHostToDevice, h2d_));
+  CK(cudaEventRecord(ev_meta_[k], h2d_));
+  h2d_bytes_ += off;
+
   // ---- onload: copy-engine H2D into staging[batch % 2] ----
   const int sb = int(batch_no_ % 2);
   if (n_on) {
@@ -562,7 +575,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
         b = std::max(b, chunk_d2h_batch_[nx.chunk_id]);
         ++run;
       }
-      if (b >= 0 && b > waited) {
+      if (b > d2h_done_upto_ && b > waited) {
         CK(cudaStreamWaitEvent(h2d_, ev_d2h_[b % kRing], 0));
         waited = b;
       }
@@ -577,8 +590,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
 
   // ---- compute stream ----
   CK(cudaEventRecord(ev_start_[k], comp_));
-  CK(cudaMemcpyAsync(db, hb, off, cudaMemcpyHostToDevice, comp_));
-  h2d_bytes_ += off;
+  CK(cudaStreamWaitEvent(comp_, ev_meta_[k], 0));
   const ReqDev* d_req = reinterpret_cast<const ReqDev*>(db);
   const uint32_t* d_pages = reinterpret_cast<const uint32_t*>(db + o_pages);
   const uint32_t* d_tok = reinterpret_cast<const uint32_t*>(db + o_tok);
@@ -703,6 +715,33 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       pick_scores_kernel<<<(ncand_total + 127) / 128, 128, 0, comp_>>>(
           static_cast<float*>(scores_.p), static_cast<const float*>(logits_.p), d_creq, d_cid, ncand_total, V);
       ++launches;
+    }
+  } else {
+    launch_tag_append(pool, d_req, d_pages, n, max_hist, g_, comp_);
+    ++launches;
+  }
+
+  // ---- offload: gather on comp (pages only ever touched here), D2H on d2h ----
+  if (n_off) {
+    int64_t waited = -1;
+    for (uint32_t j = 0; j < n_off; ++j) {
+      const int64_t b = off_slot_batch_[off_slots[j]];
+      if (b > d2h_done_upto_ && b > waited) {
+        CK(cudaStreamWaitEvent(comp_, ev_d2h_[b % kRing], 0));
+        waited = b;
+      }
+    }
+    if (prof_copy) CK(cudaEventRecord(ev_copy_[2], comp_));
+    launch_gather_chunks(static_cast<__nv_bfloat16*>(offload_.p), pool, d_chunks + n_on, d_pages, n_off, g_, comp_);
+    if (prof_copy) CK(cudaEventRecord(ev_copy_[3], comp_));
+    prof_gather_ = n_off;
+    ++launches;
+  }
+  // ---- results to the host: after the gather (kernel follows kernel on comp) and
+  // ahead of the offload D2H on the copy engine (the read-back is not queued
+  // behind this batch's offload burst) ----
+  if (value_) {
+    if (ncand_total) {
       if (scores_host_bytes_[k] < ncand_total * sizeof(float)) {
         if (scores_host_[k]) cudaFreeHost(scores_host_[k]);
         scores_host_bytes_[k] = std::max<size_t>(ncand_total * sizeof(float), 4096);
@@ -721,26 +760,8 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       CK(cudaMemcpyAsync(logits_host_[k], logits_.p, lb, cudaMemcpyDeviceToHost, comp_));
       d2h_bytes_ += lb;
     }
-  } else {
-    launch_tag_append(pool, d_req, d_pages, n, max_hist, g_, comp_);
-    ++launches;
   }
-
-  // ---- offload: gather on comp (pages only ever touched here), D2H on d2h ----
   if (n_off) {
-    int64_t waited = -1;
-    for (uint32_t j = 0; j < n_off; ++j) {
-      const int64_t b = off_slot_batch_[off_slots[j]];
-      if (b >= 0 && b > waited) {
-        CK(cudaStreamWaitEvent(comp_, ev_d2h_[b % kRing], 0));
-        waited = b;
-      }
-    }
-    if (prof_copy) CK(cudaEventRecord(ev_copy_[2], comp_));
-    launch_gather_chunks(static_cast<__nv_bfloat16*>(offload_.p), pool, d_chunks + n_on, d_pages, n_off, g_, comp_);
-    if (prof_copy) CK(cudaEventRecord(ev_copy_[3], comp_));
-    prof_gather_ = n_off;
-    ++launches;
     CK(cudaEventRecord(ev_gathered_[k], comp_));
     CK(cudaStreamWaitEvent(d2h_, ev_gathered_[k], 0));
     for (uint32_t j = 0; j < n_off; ++j) {
@@ -753,6 +774,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       off_slot_batch_[off_slots[j]] = int64_t(batch_no_);
     }
     CK(cudaEventRecord(ev_d2h_[k], d2h_));
+    d2h_rec_batch_[k] = int64_t(batch_no_);
     d2h_bytes_ += uint64_t(n_off) * chunk_bytes_;
     offload_chunks_ += n_off;
   }

@@ -88,7 +88,7 @@ class Engine {
 
   cudaStream_t comp_ = nullptr, h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_onload_[kRing], ev_scatter_[kRing], ev_gathered_[kRing], ev_d2h_[kRing],
-      ev_done_[kRing], ev_start_[kRing];
+      ev_done_[kRing], ev_start_[kRing], ev_meta_[kRing];
   std::vector<cudaEvent_t> ev_attn_;  // profiling pairs of the last batch
   cudaEvent_t ev_copy_[4] = {nullptr, nullptr, nullptr, nullptr};  // scatter start/end, gather start/end
   uint32_t prof_scatter_ = 0, prof_gather_ = 0;
@@ -138,6 +138,11 @@ class Engine {
   std::vector<uint32_t> off_free_;        // free offload slots
   std::vector<int64_t> off_slot_batch_;   // last batch that used each offload slot
   std::vector<int64_t> chunk_off_slot_;   // chunk id -> offload slot while in flight
+  // ev_d2h_ slots are reused every kRing batches: a batch that left the ring has
+  // its D2H confirmed on the host (d2h_done_upto_), so waits only ever target
+  // batches still in the ring and never alias a newer record of the same slot
+  int64_t d2h_rec_batch_[kRing] = {-1, -1, -1, -1};  // batch that last recorded ev_d2h_[k]
+  int64_t d2h_done_upto_ = -1;
   char* meta_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
   size_t meta_host_bytes_[kRing] = {0, 0, 0, 0};
   float* scores_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};

@@ -1,0 +1,76 @@
+"""In-situ kernel durations of the serving step (CUPTI activity timestamps via torch.profiler).
+
+Runs bench.py's configs[1] workload (same engine setup as tools/sweep.py), then
+records `--steps` pipelined batches under torch.profiler and prints one JSON
+line per kernel name: launches, mean/min/max device duration in us. Unlike the
+engine's CUDA-event brackets these are the kernel's own start/end timestamps,
+and unlike an ncu launch list the kernels run concurrently with the copy
+engines exactly as in the bench.
+
+  python tools/kernel_times.py [--steps 8] [--warm 24] [--config gr4_d256]
+"""
+from __future__ import annotations
+
+import argparse
+import collections
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warm", type=int, default=24)
+    ap.add_argument("--config", default="gr4_d256")
+    ap.add_argument("--users", type=int, default=0)
+    ap.add_argument("--trace", default="", help="also write a chrome trace (JSON) here")
+    args = ap.parse_args()
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    import paper_2604_22881_b200 as mtkv
+    cfg = dict(bench.CONFIGS[args.config])
+    if args.users:
+        cfg["users"] = args.users
+    kv = bench.kv_config(cfg)
+    model = mtkv.ModelConfig(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"], vocab=cfg["vocab"], seed=1)
+    B = cfg["batch"]
+    prefill, revisits = bench.make_workload(cfg, args.warm + args.steps, 0, 1)
+    tok = kv.token_kv_bytes()
+    extent_mb = -(-((cfg["history"] + 16 * cfg["delta"]) * tok) // 2**20)
+    eng = mtkv.Engine(kv, mtkv.CostModel(bus_bandwidth=55e9), mode="hierarchical", backend="value", batch_size=B,
+                      model=model, host_reserve_mb=int(1.1 * cfg["users"] * extent_mb) + 1024,
+                      host_extent_mb=extent_mb)
+    pb = max(1, 65536 // cfg["history"])
+    for i in range(0, len(prefill), pb):
+        eng.process_batch(prefill[i:i + pb])
+    batches = [mtkv.RequestBatch(revisits[i * B:(i + 1) * B]) for i in range(args.warm + args.steps)]
+    for i in range(args.warm):
+        eng.process_batch(None, packed=batches[i])
+    eng.synchronize()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(args.warm, args.warm + args.steps):
+            eng.process_batch(None, packed=batches[i])
+        eng.synchronize()
+        torch.cuda.synchronize()
+    if args.trace:
+        prof.export_chrome_trace(args.trace)
+    dur = collections.defaultdict(list)
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            dur[ev.name].append(ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total)
+    rows = sorted(dur.items(), key=lambda kv_: -sum(kv_[1]))
+    for name, d in rows:
+        print(json.dumps({"kernel": name[:90], "n": len(d), "per_step": len(d) / args.steps,
+                          "mean_us": sum(d) / len(d), "min_us": min(d), "max_us": max(d),
+                          "share_us_per_step": sum(d) / args.steps}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
