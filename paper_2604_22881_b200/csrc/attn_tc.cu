@@ -332,6 +332,9 @@ __global__ void __launch_bounds__(384, 1)
   // of tiles holding fresh keys wait for the GEMM (griddepcontrol.wait below).
   const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
   if (threadIdx.x == 0) ATTN_TR(5, 1);
+  // the gate/norm kernel (PDL) may be scheduled as CTAs of this grid retire; it
+  // waits for the whole grid (griddepcontrol.wait) before reading the partials
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 || warp == 3) {
     // ---------------- K / V producers (whole warp: lane i resolves page i) ----------------

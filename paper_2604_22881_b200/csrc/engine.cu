@@ -700,10 +700,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       gn.row_req = d_rr; gn.reqs = d_req; gn.out = X2; gn.rows = rows; gn.H = H; gn.D = g_.D;
       launch_gate_norm(gn, comp_);
       GemmArgs m1{};
-      m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = rows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID;
+      m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = rows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID; m1.pdl = true;
       if (gemm(m1, x2_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       GemmArgs m2{};
-      m2.A = MID; m2.B = w2_ + size_t(l) * d * d; m2.M = rows; m2.N = d; m2.K = d; m2.epi = Epi::Bf16; m2.out = X;
+      m2.A = MID; m2.B = w2_ + size_t(l) * d * d; m2.M = rows; m2.N = d; m2.K = d; m2.epi = Epi::Bf16; m2.out = X; m2.pdl = true;
       if (gemm(m2, mid_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       launches += 5;
     }

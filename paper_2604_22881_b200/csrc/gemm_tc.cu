@@ -9,7 +9,8 @@
 // One CTA per 128 x BN output tile (128 threads): warp 0 streams A / W k-blocks
 // with TMA (128-B swizzle, 2-stage ring; several CTAs per SM), one elected lane of warp 1 issues
 // tcgen05.mma kind::f16 (A K-major, W MN-major), all 4 warps drain TMEM
-// (tcgen05.ld, one output row per thread) through the fused epilogue.
+// (tcgen05.ld, one output row per thread) through the fused epilogue into a
+// swizzled smem tile that whole warps store as contiguous row segments.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -71,7 +72,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 }  // namespace gtc
 
@@ -107,9 +108,12 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  // every CTA of this grid is resident: let the next kernel (attention, launched
-  // with programmatic serialization) start its prologue on SMs as they free up
+  // every CTA of this grid is resident: let the next kernel (launched with
+  // programmatic serialization) start its prologue on SMs as they free up
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // PDL launch (a.pdl): the prologue above overlapped the predecessor; its
+  // outputs (our A operand) are complete and visible after this (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     for (int kb = 0; kb < nk; ++kb) {
@@ -137,56 +141,57 @@ __global__ void __launch_bounds__(128)
     }
     commit(done);
   }
-  // epilogue: thread t owns output row m0 + t (TMEM lane t)
+  // epilogue: TMEM (thread t = output row m0 + t) -> registers (silu, bf16) ->
+  // a swizzled bf16 tile in the freed pipeline smem -> row segments stored by
+  // whole warps (16-B per lane, 256 contiguous bytes per row of a 128-wide
+  // tile), so every global store instruction writes full sectors
   __syncwarp();
-  mbar_wait(done, 0);
+  mbar_wait(done, 0);  // all MMAs complete: the TMA stages are no longer read
   __syncwarp();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + int(threadIdx.x);
+  constexpr int CPR = BN / 8;  // 16-B chunks per tile row (a multiple of 8)
+  uint4* tile = reinterpret_cast<uint4*>(smem);
+  const uint32_t trow = threadIdx.x;
   const uint32_t taddr = tmem + ((32u * warp) << 16);
+  const bool act = g.epi != Epi::Bf16;  // Proj and SiluBf16 apply silu
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     float v[32];
     tmem_ld32(taddr + c * 32, v);
-    if (row >= g.M) continue;
-    const int col0 = n0 + c * 32;
-    if (g.epi == Epi::Proj) {
-      // the 32 columns lie in one of u | q | k | v when d % 32 == 0
-      const uint32_t part = uint32_t(col0) / g.d, w = uint32_t(col0) % g.d;
-      __nv_bfloat16* dst = part == 0   ? g.out_u + size_t(row) * g.d + w
-                           : part == 1 ? g.out_q + size_t(row) * g.d + w
-                                       : g.pool + g.layer_base + g.kv_off[row] + (part == 3 ? g.kv_stride : 0) + w;
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 pk;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(silu(v[i]), silu(v[i + 1]));
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(silu(v[i + 2]), silu(v[i + 3]));
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(silu(v[i + 4]), silu(v[i + 5]));
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(silu(v[i + 6]), silu(v[i + 7]));
-        pk.x = *reinterpret_cast<uint32_t*>(&h0);
-        pk.y = *reinterpret_cast<uint32_t*>(&h1);
-        pk.z = *reinterpret_cast<uint32_t*>(&h2);
-        pk.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(dst + i) = pk;
-      }
-    } else {
-      const bool act = g.epi == Epi::SiluBf16;
-      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g.out) + size_t(row) * g.N + col0;
+    for (int i = 0; i < 4; ++i) {
+      float x[8];
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 pk;
-        float x[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = act ? silu(v[i + j]) : v[i + j];
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]), h1 = __floats2bfloat162_rn(x[2], x[3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(x[4], x[5]), h3 = __floats2bfloat162_rn(x[6], x[7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&h0);
-        pk.y = *reinterpret_cast<uint32_t*>(&h1);
-        pk.z = *reinterpret_cast<uint32_t*>(&h2);
-        pk.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(dst + i) = pk;
-      }
+      for (int j = 0; j < 8; ++j) x[j] = act ? silu(v[8 * i + j]) : v[8 * i + j];
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]), h1 = __floats2bfloat162_rn(x[2], x[3]);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(x[4], x[5]), h3 = __floats2bfloat162_rn(x[6], x[7]);
+      uint4 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&h0);
+      pk.y = *reinterpret_cast<uint32_t*>(&h1);
+      pk.z = *reinterpret_cast<uint32_t*>(&h2);
+      pk.w = *reinterpret_cast<uint32_t*>(&h3);
+      tile[trow * CPR + ((c * 4 + i) ^ (trow & 7))] = pk;
     }
+  }
+  __syncwarp();  // each warp stores the 32 rows it staged
+  constexpr int RPI = 32 / CPR;  // rows per warp instruction
+  const int ch = int(lane) % CPR;
+  const int col = n0 + ch * 8;
+  // Proj: the column's part (u | q | k | v) and offset within it; k / v rows go to the pool
+  const uint32_t part = g.epi == Epi::Proj ? uint32_t(col) / g.d : 0u, w = g.epi == Epi::Proj ? uint32_t(col) % g.d : 0u;
+#pragma unroll 4
+  for (int rr = int(lane) / CPR; rr < 32; rr += RPI) {
+    const int tr = int(warp) * 32 + rr, row = m0 + tr;
+    if (row >= g.M) break;
+    const uint4 val = tile[tr * CPR + (ch ^ (tr & 7))];
+    __nv_bfloat16* dst;
+    if (g.epi == Epi::Proj)
+      dst = part == 0   ? g.out_u + size_t(row) * g.d + w
+            : part == 1 ? g.out_q + size_t(row) * g.d + w
+                        : g.pool + g.layer_base + g.kv_off[row] + (part == 3 ? g.kv_stride : 0) + w;
+    else
+      dst = static_cast<__nv_bfloat16*>(g.out) + size_t(row) * g.N + col;
+    *reinterpret_cast<uint4*>(dst) = val;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -216,7 +221,7 @@ static bool encode(CUtensorMap* map, const void* base, uint64_t cols, uint64_t r
 }
 
 bool gemm_tc_supported(const GemmArgs& a) {
-  return !a.row_idx && a.epi != Epi::F32 && a.K % 64 == 0 && a.N % 64 == 0 && (a.epi != Epi::Proj || a.d % 32 == 0);
+  return !a.row_idx && a.epi != Epi::F32 && a.K % 64 == 0 && a.N % 64 == 0 && (a.epi != Epi::Proj || a.d % 8 == 0);
 }
 
 template <int BN>
@@ -227,8 +232,17 @@ static void launch_bn(const CUtensorMap& am, const CUtensorMap& wm, const GemmAr
     cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     set = true;
   }
-  const dim3 grid(a.N / BN, (a.M + BM - 1) / BM);
-  gemm_tc_kernel<BN><<<grid, 128, smem, s>>>(am, wm, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.N / BN, (a.M + BM - 1) / BM);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN>, am, wm, a);
 }
 
 // tensor maps are cached per (buffer, shape, box): activation workspaces and

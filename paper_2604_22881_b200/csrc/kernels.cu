@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 // ------------------------------------------------------------------- GEMM ---
 // 64x64x32 block tile, 4 warps (2x2, 32x32 each), double-buffered smem.
@@ -476,6 +476,9 @@ __device__ __forceinline__ float gate_merge_col(const GateArgs& a, const AttnSeg
 
 template <int E>  // contiguous columns per lane
 __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) {
+  // launched with PDL behind the attention: wait for its partials, let the MLP GEMM launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int wid = threadIdx.x / 32;
   const int row = blockIdx.x * GATE_WARPS + wid;
   const int lane = threadIdx.x & 31;
@@ -487,6 +490,27 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
   float sum = 0.f;
   if constexpr (E > 0) {
     const uint32_t j0 = lane * E, h = j0 / a.D, c0 = j0 % a.D;
+    // the gate operand does not depend on the merge: its load overlaps the slot reads
+    float ug[E];
+    {
+      const __nv_bfloat16* up = a.u + (size_t)row * d + j0;
+      if constexpr (E % 8 == 0) {
+#pragma unroll
+        for (int e = 0; e < E; e += 8) {
+          const uint4 pk = *reinterpret_cast<const uint4*>(up + e);
+          const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&pk);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(p2[k]);
+            ug[e + 2 * k] = f.x;
+            ug[e + 2 * k + 1] = f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) ug[e] = __bfloat162float(up[e]);
+      }
+    }
     const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
     float mx = -INFINITY;
     for (uint32_t k = 0; k < sg.n_parts; ++k) mx = fmaxf(mx, a.part_lse[(size_t)(sg.part_base + k) * a.bm + ri]);
@@ -513,11 +537,10 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
       }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;
-    const __nv_bfloat16* up = a.u + (size_t)row * d + j0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const float o = acc[e] * inv;
-      x[e] = (o / (1.0f + expf(-o))) * __bfloat162float(up[e]);
+      x[e] = silu_f(o) * ug[e];
       sum += x[e];
     }
   } else {
@@ -529,7 +552,7 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
       const uint32_t h = j / a.D;
       const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
       const float o = gate_merge_col(a, sg, ri, j % a.D);
-      x[e] = (o / (1.0f + expf(-o))) * __bfloat162float(a.u[(size_t)row * d + j]);
+      x[e] = silu_f(o) * __bfloat162float(a.u[(size_t)row * d + j]);
       sum += x[e];
     }
   }
@@ -548,8 +571,26 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
   const float inv = 1.0f / sqrtf(var + 1e-6f);
   if constexpr (E > 0) {
     __nv_bfloat16* op = a.out + (size_t)row * d + lane * E;
+    if constexpr (E % 8 == 0) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) op[e] = __float2bfloat16((x[e] - mean) * inv * a.ln_scale[lane * E + e]);
+      for (int e = 0; e < E; e += 8) {
+        const float4 s0 = *reinterpret_cast<const float4*>(a.ln_scale + lane * E + e);
+        const float4 s1 = *reinterpret_cast<const float4*>(a.ln_scale + lane * E + e + 4);
+        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        uint4 pk;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn((x[e + 2 * k] - mean) * inv * sc[2 * k],
+                                                          (x[e + 2 * k + 1] - mean) * inv * sc[2 * k + 1]);
+          pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        *reinterpret_cast<uint4*>(op + e) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) op[e] = __float2bfloat16((x[e] - mean) * inv * a.ln_scale[lane * E + e]);
+    }
   } else {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
@@ -562,18 +603,26 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
 void launch_gate_norm(const GateArgs& a, cudaStream_t s) {
   if (a.rows == 0) return;
   const uint32_t d = a.H * a.D, E = d % 32 == 0 ? d / 32 : 0;
-  const dim3 grid((a.rows + GATE_WARPS - 1) / GATE_WARPS), block(GATE_WARPS * 32);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.rows + GATE_WARPS - 1) / GATE_WARPS);
+  cfg.blockDim = dim3(GATE_WARPS * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (E && a.D % E == 0) {
     switch (E) {
-      case 1: gate_norm_kernel<1><<<grid, block, 0, s>>>(a); return;
-      case 2: gate_norm_kernel<2><<<grid, block, 0, s>>>(a); return;
-      case 4: gate_norm_kernel<4><<<grid, block, 0, s>>>(a); return;
-      case 8: gate_norm_kernel<8><<<grid, block, 0, s>>>(a); return;
-      case 16: gate_norm_kernel<16><<<grid, block, 0, s>>>(a); return;
+      case 1: cudaLaunchKernelEx(&cfg, gate_norm_kernel<1>, a); return;
+      case 2: cudaLaunchKernelEx(&cfg, gate_norm_kernel<2>, a); return;
+      case 4: cudaLaunchKernelEx(&cfg, gate_norm_kernel<4>, a); return;
+      case 8: cudaLaunchKernelEx(&cfg, gate_norm_kernel<8>, a); return;
+      case 16: cudaLaunchKernelEx(&cfg, gate_norm_kernel<16>, a); return;
       default: break;
     }
   }
-  gate_norm_kernel<0><<<grid, block, 0, s>>>(a);
+  cudaLaunchKernelEx(&cfg, gate_norm_kernel<0>, a);
 }
 
 // -------------------------------------------------------- scatter/gather ---

@@ -81,6 +81,8 @@ struct GemmArgs {
   uint64_t layer_base;      // element offset of the layer plane
   uint32_t d;               // hidden width (Proj: N = 4d)
   uint32_t kv_stride;       // V offset from K = page_size * d
+  bool pdl = false;         // launch with programmatic stream serialization (the kernel
+                            // waits for its predecessor before touching global data)
 };
 
 void launch_gemm(const GemmArgs& a, cudaStream_t s);
@@ -111,7 +113,7 @@ struct AttnArgs {
 constexpr int kTraceCtas = 64, kTraceTiles = 96, kTraceKinds = 12;
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 
-struct GateArgs {  // split combine + silu(o) * u + layer norm -> bf16
+struct GateArgs {  // split combine + silu(o) * u + layer norm -> bf16 (launched with PDL)
   const float* part_o;
   const float* part_lse;
   const AttnSeg* segs;

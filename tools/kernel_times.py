@@ -65,6 +65,21 @@ def main():
     for ev in prof.events():
         if ev.device_type == torch.autograd.DeviceType.CUDA:
             dur[ev.name].append(ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total)
+    # per batch: the layer stack's device span, embed start -> scoring kernel end
+    # (PDL-launched kernels start early and wait, so their own durations overlap
+    # their predecessors'; the span is the honest per-batch compute time)
+    kev = sorted((e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA),
+                 key=lambda e: e.time_range.start)
+    spans, t_embed = [], None
+    for e in kev:
+        if "embed_kernel" in e.name:
+            t_embed = e.time_range.start
+        elif "pick_scores" in e.name and t_embed is not None:
+            spans.append(e.time_range.end - t_embed)
+            t_embed = None
+    if spans:
+        print(json.dumps({"layer_stack_span_us": {"mean": sum(spans) / len(spans), "min": min(spans),
+                                                  "max": max(spans), "batches": len(spans)}}), flush=True)
     rows = sorted(dur.items(), key=lambda kv_: -sum(kv_[1]))
     for name, d in rows:
         print(json.dumps({"kernel": name[:90], "n": len(d), "per_step": len(d) / args.steps,
