@@ -650,6 +650,11 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       ga.A = X; ga.B = w_in_ + size_t(l) * d * 4 * d; ga.M = rows; ga.N = 4 * d; ga.K = d;
       ga.epi = Epi::Proj; ga.out_u = U; ga.out_q = Q; ga.pool = pool; ga.kv_off = d_kv;
       ga.layer_base = size_t(l) * g_.num_pages * 2 * S * d; ga.d = d; ga.kv_stride = S * d;
+      // PDL: the prologue overlaps the previous layer's MLP; the epilogue's writes
+      // (U, Q, this layer's pool plane) follow griddepcontrol.wait, by which time
+      // every earlier reader of U / Q / part_o has completed (each PDL kernel of
+      // the chain waited for its predecessor)
+      ga.pdl = true;
       if (prof) CK(cudaEventRecord(ev_attn_[2 * g_.L + 2 * l], comp_));
       if (gemm(ga, x_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       if (prof) CK(cudaEventRecord(ev_attn_[2 * g_.L + 2 * l + 1], comp_));
