@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) ATTN_TR(5, 1);
   // the gate/norm kernel (PDL) may be scheduled as CTAs of this grid retire; it
   // waits for the whole grid (griddepcontrol.wait) before reading the partials
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 || warp == 3) {
     // ---------------- K / V producers (whole warp: lane i resolves page i) ----------------
@@ -805,8 +805,14 @@ static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, c
 void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
                          const AttnArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
-  if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, part_map, a, s);
-  else launch_tc_d<128>(pool_map, q_map, part_map, a, s);
+  static const bool no_trigger = [] {  // MTKV_ATTN_TRIGGER=0: A/B switch for the early PDL release
+    const char* e = std::getenv("MTKV_ATTN_TRIGGER");
+    return e && e[0] == '0';
+  }();
+  AttnArgs b = a;
+  if (no_trigger) b.trigger = 0;
+  if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, part_map, b, s);
+  else launch_tc_d<128>(pool_map, q_map, part_map, b, s);
 }
 
 }  // namespace mtkv_b200

@@ -109,6 +109,7 @@ struct AttnArgs {
   float scale_log2;         // log2(e) / sqrt(D)
   uint32_t bq;              // query rows per tile: 64 or 128 (items enumerate tiles of bq)
   unsigned long long* trace;  // optional per-CTA event timestamps (MTKV_ATTN_TRACE), else null
+  uint32_t trigger = 1;       // tcgen05 path: release the PDL dependent (gate_norm) at CTA start
 };
 constexpr int kTraceCtas = 64, kTraceTiles = 96, kTraceKinds = 12;
 void launch_attention(const AttnArgs& a, cudaStream_t s);
