@@ -20,7 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I" + CSRC,
           "-I" + os.path.join(os.path.dirname(HERE), "include")]
-CUDA_FLAGS = ARCH + ["-Xptxas", "-v", "--expt-relaxed-constexpr"]
+CUDA_FLAGS = ARCH + ["-Xptxas", "-v", "--expt-relaxed-constexpr"] + os.environ.get("MTKV_NVCC_EXTRA", "").split()
+# MTKV_NVCC_EXTRA: extra nvcc flags for diagnostic builds (e.g. -DMTKV_ATTN_WATCHDOG)
 
 
 def sources():

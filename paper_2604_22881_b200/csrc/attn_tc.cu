@@ -34,6 +34,7 @@
 //   V    : MN-major [keys][64-dim blocks],  SBO = 1024 B, LBO = one block
 // TMEM columns: S/P buffers (2 x 128 fp32) | O (D fp32) | Q (D/2).
 #include <cuda.h>
+#include <cstdio>
 #include <cudaTypedefs.h>
 
 #include <cmath>
@@ -59,17 +60,58 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
 }
-// try_wait with a suspend-time hint: the waiting warp sleeps in hardware until
-// the phase completes instead of re-polling (polling warps steal issue slots
-// from the softmax warps sharing their SM sub-partition)
+#ifdef MTKV_WATCHDOG
+// diagnostic build (MTKV_NVCC_EXTRA=-DMTKV_WATCHDOG): a wait still pending after
+// 0.2 s reports the barrier and the waiting warp, and traps after 1 s
+#define WD_NAME "attn"
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  bool told = false;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(s32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!told && t - t0 > 200000000ull) {
+      told = true;
+      if (threadIdx.x % 32 == 0)
+        printf("%s watchdog: cta %d,%d thread %d bar 0x%x parity %u\n", WD_NAME, blockIdx.x, blockIdx.y, threadIdx.x,
+               s32(b), parity);
+    }
+    if (t - t0 > 1000000000ull) __trap();
+  }
 }
+#else
+// Polling try_wait (no suspend-time hint). MTKV_SUSPEND_NS > 0 builds the
+// hinted form for A/B runs: with a 1 ms hint, small test batches stalled for
+// minutes (waits resumed long after their phase completed), so the default polls.
+#ifndef MTKV_SUSPEND_NS
+#define MTKV_SUSPEND_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  if constexpr (MTKV_SUSPEND_NS > 0) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
+        "r"(parity), "r"(uint32_t(MTKV_SUSPEND_NS))
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
+        "r"(parity)
+        : "memory");
+  }
+}
+#endif
 __device__ __forceinline__ bool mbar_ready(uint64_t* b, uint32_t parity) {
   uint32_t ok;
   asm volatile(

@@ -12,6 +12,7 @@
 // (tcgen05.ld, one output row per thread) through the fused epilogue into a
 // swizzled smem tile that whole warps store as contiguous row segments.
 #include <cuda.h>
+#include <cstdio>
 #include <cudaTypedefs.h>
 
 #include <vector>
@@ -31,14 +32,43 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
 }
+#ifdef MTKV_WATCHDOG
+// diagnostic build (MTKV_NVCC_EXTRA=-DMTKV_WATCHDOG): a wait still pending after
+// 0.2 s reports the barrier and the waiting warp, and traps after 1 s
+#define WD_NAME "gemm"
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  bool told = false;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(s32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!told && t - t0 > 200000000ull) {
+      told = true;
+      if (threadIdx.x % 32 == 0)
+        printf("%s watchdog: cta %d,%d thread %d bar 0x%x parity %u\n", WD_NAME, blockIdx.x, blockIdx.y, threadIdx.x,
+               s32(b), parity);
+    }
+    if (t - t0 > 1000000000ull) __trap();
+  }
+}
+#else
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {  // polling (see attn_tc.cu)
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n}\n" ::"r"(s32(b)),
-      "r"(parity), "r"(1000000u)
+      "r"(parity)
       : "memory");
 }
+#endif
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -281,9 +311,9 @@ int launch_gemm_tc(const GemmArgs& a, uint64_t a_rows_alloc, cudaStream_t s) {
   const CUtensorMap* wmp = cached_map(a.B, a.N, a.K, 64, BK);
   if (!amp || !wmp) return -1;
   const CUtensorMap am = *amp, wm = *wmp;
-  // wide N: 128-column tiles; narrow N (MLP, d): 64-column tiles for more CTAs
   // wide N (projection, 4d): 128-column tiles (measured 16.5 us vs 18.7 us with
-  // 64-column tiles on the bench layer); narrow N (MLP, d): 64-column tiles
+  // 64-column tiles, and a 415 vs 439 us layer-stack span against 256-column
+  // tiles at 2 CTAs per SM); narrow N (MLP, d): 64-column tiles
   if (a.N >= 1024) launch_bn<128>(am, wm, a, s);
   else launch_bn<64>(am, wm, a, s);
   return 0;
