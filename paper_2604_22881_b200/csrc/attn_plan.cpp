@@ -100,7 +100,11 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
         for (uint32_t sg = lists[k][li], lo = spans[k][li].first, hi = spans[k][li].second; lo < hi;) {
           if (room == 0) { ++c; room = quota; }
           const uint32_t take = uint32_t(std::min<uint64_t>(hi - lo, room));
-          R[k][std::min(c, groups - 1)].push_back(AttnPiece{sg, lo, lo + take, 0});
+          AttnPiece pc{};
+          pc.seg = sg;
+          pc.lo = lo;
+          pc.hi = lo + take;
+          R[k][std::min(c, groups - 1)].push_back(pc);
           lo += take;
           room -= take;
         }
@@ -121,7 +125,22 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
       P.n_slots += npc[sg];
     }
     std::vector<uint32_t> used(P.segs.size(), 0);
-    for (AttnPiece& pc : P.pieces) pc.part = P.segs[pc.seg].part_base + used[pc.seg]++;
+    for (AttnPiece& pc : P.pieces) {
+      pc.part = P.segs[pc.seg].part_base + used[pc.seg]++;
+      const AttnSeg& sg = P.segs[pc.seg];
+      const ReqDev& R = reqs[sg.req];
+      pc.head = sg.head;
+      pc.qtile = sg.qtile;
+      pc.q_row0 = R.q_row0;
+      pc.n_q = R.n_q;
+      pc.n_hist = R.n_hist;
+      pc.n_cand = R.n_cand;
+      pc.pages_off = R.pages_off;
+      pc.scratch_off = R.scratch_off;
+      pc.n_scratch = R.n_scratch;
+      pc.start = R.start;
+      pc.dep_start = R.dep_start;
+    }
     return;
   }
   // mma.sync path: 64/128-row query tiles over positions, 512-key splits for

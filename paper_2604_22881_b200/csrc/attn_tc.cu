@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(384, 1)
   const PoolGeom& g = a.g;
   const uint32_t S = g.S;
   if (threadIdx.x == 0) ATTN_TR(5, 0);
+  // this CTA's piece range (read ahead of the barrier / TMEM setup)
+  const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
 
   if (threadIdx.x == 0) {
     // a K stage is released by the 8 softmax warps once they hold S (so the S
@@ -372,7 +374,6 @@ __global__ void __launch_bounds__(384, 1)
   // Everything before it in the stream (batch metadata, the cached prefix in the
   // pool, the previous consumer of part_o) is complete, so only reads of Q and
   // of tiles holding fresh keys wait for the GEMM (griddepcontrol.wait below).
-  const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
   if (threadIdx.x == 0) ATTN_TR(5, 1);
   // the gate/norm kernel (PDL) may be scheduled as CTAs of this grid retire; it
   // waits for the whole grid (griddepcontrol.wait) before reading the partials
@@ -390,16 +391,14 @@ __global__ void __launch_bounds__(384, 1)
     bool dep_done = false;        // griddepcontrol.wait executed
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
-      const AttnSeg sg = a.segs[P.seg];
-      const ReqDev R = a.reqs[sg.req];
-      const uint64_t KA = R.start + R.n_hist;
+      const uint64_t KA = P.start + P.n_hist;
       const uint32_t user_pages = uint32_t((KA + S - 1) / S);
-      const uint32_t col = sg.head * D;
+      const uint32_t col = P.head * D;
       auto row_of = [&](uint64_t lp) -> int {  // pool row of a logical page's K slice
         uint32_t page;
-        if (lp < user_pages) page = a.pages[R.pages_off + uint32_t(lp)];
-        else if (lp - user_pages < R.n_scratch && (lp - user_pages) * S < R.n_cand)
-          page = a.pages[R.scratch_off + uint32_t(lp - user_pages)];
+        if (lp < user_pages) page = a.pages[P.pages_off + uint32_t(lp)];
+        else if (lp - user_pages < P.n_scratch && (lp - user_pages) * S < P.n_cand)
+          page = a.pages[P.scratch_off + uint32_t(lp - user_pages)];
         else return -int(S) * 4;  // out of bounds -> TMA zero fill
         return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
       };
@@ -410,7 +409,7 @@ __global__ void __launch_bounds__(384, 1)
           cache_t0 = t;
           rows_cache = row_of(uint64_t(t) * ppt + lane);
         }
-        if (!dep_done && uint64_t(t + 1) * BN > R.dep_start) {  // tile holds keys this layer's GEMM appends
+        if (!dep_done && uint64_t(t + 1) * BN > P.dep_start) {  // tile holds keys this layer's GEMM appends
           asm volatile("griddepcontrol.wait;" ::: "memory");
           dep_done = true;
         }
@@ -440,8 +439,6 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t k = 0;
       for (uint32_t pc = pb; pc < pe; ++pc, ++k) {
         const AttnPiece P = a.pieces[pc];
-        const AttnSeg sg = a.segs[P.seg];
-        const ReqDev R = a.reqs[sg.req];
         const uint32_t qb = k & 1;
         if (k >= 2) {
           mbar_wait(&q_empty[qb], ((k >> 1) - 1) & 1);
@@ -450,7 +447,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_expect_tx(&q_full[qb], Q_BYTES);
 #pragma unroll
         for (int b = 0; b < NB; ++b)
-          tma_load_2d(sQ + qb * Q_BYTES + b * QBLK, &q_map, int(sg.head * D + 64 * b), int(R.q_row0 + sg.qtile * BM),
+          tma_load_2d(sQ + qb * Q_BYTES + b * QBLK, &q_map, int(P.head * D + 64 * b), int(P.q_row0 + P.qtile * BM),
                       &q_full[qb]);
       }
     }
@@ -559,19 +556,17 @@ __global__ void __launch_bounds__(384, 1)
     };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
-      const AttnSeg sg = a.segs[P.seg];
-      const ReqDev R = a.reqs[sg.req];
-      const uint64_t KA = R.start + R.n_hist;
+      const uint64_t KA = P.start + P.n_hist;
       const uint64_t KAp = (KA + S - 1) / S * S;
-      const uint32_t q0 = sg.qtile * BM;
-      const uint32_t q_end = min(R.n_q, q0 + BM);
-      const uint64_t pos_last = R.start + q_end - 1;
+      const uint32_t q0 = P.qtile * BM;
+      const uint32_t q_end = min(P.n_q, q0 + BM);
+      const uint64_t pos_last = P.start + q_end - 1;
       const uint64_t k_vis = pos_last >= KA ? KAp + (pos_last - KA + 1) : pos_last + 1;
       const uint64_t k_hi = min(k_vis, uint64_t(P.hi) * BN);
-      const uint64_t pos_r = R.start + q0 + r;
+      const uint64_t pos_r = P.start + q0 + r;
       // valid keys of this row: user keys [0, u_end), candidate keys [KAp, c_end)
       const uint64_t u_end = min(min(KA, k_hi), pos_r + 1);
-      const uint64_t c_end = pos_r >= KA ? min(min(KAp + R.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
+      const uint64_t c_end = pos_r >= KA ? min(min(KAp + P.n_cand, KAp + (pos_r - KA + 1)), k_hi) : KAp;
       // the same bounds relative to this warpgroup's first key of the piece, clamped (32-bit per tile)
       const uint64_t kb0 = uint64_t(P.lo) * BN + wg * HC;
       const int64_t span = int64_t(P.hi - P.lo) * BN;

@@ -50,9 +50,15 @@ struct AttnSeg {
   uint32_t part_base, n_parts;
 };
 // tcgen05 path: a piece = key tiles [lo, hi) of one segment, run by one CTA of
-// the persistent kernel; its partial result goes to slot `part`.
-struct AttnPiece {
+// the persistent kernel; its partial result goes to slot `part`. The segment's
+// and request's fields the kernel needs are copied in (one load per piece
+// instead of a piece -> segment -> request chain of dependent loads).
+struct alignas(16) AttnPiece {
   uint32_t seg, lo, hi, part;
+  uint32_t head, qtile, q_row0, n_q;      // segment / request
+  uint32_t n_hist, n_cand, pages_off, scratch_off;
+  uint32_t n_scratch, pad_;
+  uint64_t start, dep_start;
 };
 struct AttnItem {  // mma.sync path: one CTA = (request, head, query tile, key split)
   uint32_t req, head, qtile, split;
