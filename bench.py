@@ -244,7 +244,8 @@ def run_b200(args, cfg):
                              seed=1)
     B, K = cfg["batch"], args.steps
     warm = args.warmup + max(args.warmup, 2 * K)  # long warm-up: timed phases see the steady state
-    prefill, revisits = make_workload(cfg, warm + 3 * K, rank, world)
+    N_OVL = 8  # phase D batches (compute / transfer overlap under CUPTI)
+    prefill, revisits = make_workload(cfg, warm + 3 * K + N_OVL, rank, world)
     # pinned host store sized for the run up front (no cudaHostAlloc while serving)
     tok_bytes = kv.token_kv_bytes()
     # one pinned extent per user sized to its persisted prefix over the run, so a
@@ -259,7 +260,7 @@ def run_b200(args, cfg):
     pb = max(1, 65536 // cfg["history"])
     for i in range(0, len(prefill), pb):
         eng.process_batch(prefill[i:i + pb])
-    batches = [revisits[i * B:(i + 1) * B] for i in range(warm + 3 * K)]
+    batches = [revisits[i * B:(i + 1) * B] for i in range(warm + 3 * K + N_OVL)]
     packed = [mtkv.RequestBatch(b) for b in batches]
     for i in range(warm):
         eng.process_batch(None, packed=packed[i])
@@ -342,6 +343,25 @@ def run_b200(args, cfg):
     assert n_read == K
     phase_c = _phase(e0, eng.report(), K, B)
 
+    # ---- phase D (untimed): compute / transfer overlap of the next batches under CUPTI ----
+    overlap = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import kernel_times
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for i in range(k1 + K, k1 + K + N_OVL):
+                eng.process_batch(None, packed=packed[i])
+            eng.synchronize()
+            torch.cuda.synchronize()
+        ov = kernel_times.overlap_stats(prof.events())
+        overlap = {"compute_hidden_frac": ov["compute_hidden_frac"], "h2d_busy_frac": ov["h2d_busy_frac"],
+                   "batches": N_OVL,
+                   "note": "CUPTI timestamps: fraction of kernel time with an H2D copy in flight; H2D engine busy "
+                           "fraction of the span"}
+    except Exception as e:  # profiler unavailable: the line says so
+        overlap = {"unavailable": f"{type(e).__name__}: {e}"[:120]}
+
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -412,6 +432,7 @@ def run_b200(args, cfg):
                       "frac": phase_a["h2d_bytes_per_step"] * K / elapsed / 1e9 / H2D_PEAK_GBS,
                       "d2h_GBs": phase_a["d2h_bytes_per_step"] * K / elapsed / 1e9,
                       "note": "timed phase A; the step is host-link bound when frac ~ 1"},
+        "overlap": overlap,
         "control_plane": {"planner": args.planner,
                           "plan_ms_per_batch": float(np.mean(plan_ms)) if plan_ms else None,
                           "device_planner_kernel_us": float(np.mean(ctl_ms)) * 1e3 if args.planner == "device" else None,

@@ -23,6 +23,47 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 
+def _union(iv):
+    out = []
+    for a, b in sorted(iv):
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def overlap_stats(events) -> dict:
+    """Compute/transfer overlap over a profiled window (torch.profiler CUDA
+    events): the fraction of device compute time (union of kernel intervals)
+    that ran while a host->device copy was in flight, and how busy the H2D
+    engine was. compute_hidden_frac ~ 1 means the onload traffic fully overlaps
+    the compute (or, when the link is the bottleneck, the compute is hidden).
+    Kernel time outside [first copy start, last copy end] — the pipeline drain
+    after the window's last onload — is not counted (it has no next batch's
+    copy to hide behind)."""
+    import torch
+    cuda = [e for e in events if e.device_type == torch.autograd.DeviceType.CUDA]
+    h = _union([(e.time_range.start, e.time_range.end) for e in cuda if "HtoD" in e.name])
+    h_lo, h_hi = (h[0][0], h[-1][1]) if h else (0.0, 0.0)
+    k = _union([(max(e.time_range.start, h_lo), min(e.time_range.end, h_hi)) for e in cuda
+                if not e.name.startswith("Memcpy") and not e.name.startswith("Memset")
+                and e.time_range.end > h_lo and e.time_range.start < h_hi])
+    inter, j = 0.0, 0
+    for a, b in k:
+        while j < len(h) and h[j][1] <= a:
+            j += 1
+        jj = j
+        while jj < len(h) and h[jj][0] < b:
+            inter += max(0.0, min(b, h[jj][1]) - max(a, h[jj][0]))
+            jj += 1
+    kb = sum(b - a for a, b in k)
+    hb = sum(b - a for a, b in h)
+    return {"compute_busy_us": kb, "h2d_busy_us": hb, "span_us": h_hi - h_lo,
+            "compute_hidden_frac": inter / kb if kb else None,
+            "h2d_busy_frac": hb / (h_hi - h_lo) if h_hi > h_lo else None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=8)
@@ -77,6 +118,7 @@ def main():
         elif "pick_scores" in e.name and t_embed is not None:
             spans.append(e.time_range.end - t_embed)
             t_embed = None
+    print(json.dumps({"overlap": overlap_stats(prof.events())}), flush=True)
     if spans:
         print(json.dumps({"layer_stack_span_us": {"mean": sum(spans) / len(spans), "min": min(spans),
                                                   "max": max(spans), "batches": len(spans)}}), flush=True)

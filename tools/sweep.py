@@ -7,7 +7,8 @@ Both use bench.py's workload (configs[1] model: 4 layers, d=256, 4K-token
 histories, 64 new tokens + 8 candidates per request, lognormal revisits) and
 time the device with CUDA events over K batches after a warm-up; the per-mode
 numbers are the same metric as bench.py (requests/s, tokens/s, p50/p99 batch ms,
-hit ratios, host-link bytes). Multi-GPU points are bench.py under torchrun
+hit ratios, host-link bytes), plus the compute/transfer overlap of a CUPTI
+replay of the timed batches (fraction of kernel time with an H2D copy in flight). Multi-GPU points are bench.py under torchrun
 (user-sharded, no collective: every rank runs this exact per-GPU workload).
 """
 from __future__ import annotations
@@ -34,7 +35,8 @@ def run_mode(cfg: dict, mode: str, steps: int, warm: int, pool_frac: float | Non
     kv = bench.kv_config(cfg)
     model = mtkv.ModelConfig(num_layers=cfg["L"], num_heads=cfg["H"], head_dim=cfg["D"], vocab=cfg["vocab"], seed=1)
     B = cfg["batch"]
-    prefill, revisits = bench.make_workload(cfg, warm + steps, 0, 1)
+    n_extra = 16  # fresh batches after the timed ones: 8 profiled (overlap), 8 for per-batch latency
+    prefill, revisits = bench.make_workload(cfg, warm + steps + n_extra, 0, 1)
     tok = kv.token_kv_bytes()
     extent_mb = -(-((cfg["history"] + 16 * cfg["delta"]) * tok) // 2**20)
     host_mb = int(1.1 * cfg["users"] * extent_mb) + 1024 if mode == "hierarchical" else 0
@@ -47,7 +49,7 @@ def run_mode(cfg: dict, mode: str, steps: int, warm: int, pool_frac: float | Non
     else:  # the recompute engine still needs each user's token history
         for i in range(0, len(prefill), 4):
             eng.process_batch(prefill[i:i + 4])
-    batches = [mtkv.RequestBatch(revisits[i * B:(i + 1) * B]) for i in range(warm + steps)]
+    batches = [mtkv.RequestBatch(revisits[i * B:(i + 1) * B]) for i in range(warm + steps + n_extra)]
     for i in range(warm):
         eng.process_batch(None, packed=batches[i])
     eng.synchronize()
@@ -63,9 +65,22 @@ def run_mode(cfg: dict, mode: str, steps: int, warm: int, pool_frac: float | Non
     el = t0.elapsed_time(t1) / 1e3
     r1 = eng.report()
     ph = bench._phase(r0, r1, steps, B)
+    # compute/transfer overlap under CUPTI (tools/kernel_times.overlap_stats) on the
+    # next 8 batches of the same stream (fresh requests, not a replay)
+    from torch.profiler import ProfilerActivity, profile
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import kernel_times
+    tb = warm + steps
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(tb, tb + 8):
+            eng.process_batch(None, packed=batches[i])
+        eng.synchronize()
+        torch.cuda.synchronize()
+    ov = kernel_times.overlap_stats(prof.events())
+    # per-batch latency (enqueue -> done, one batch in flight) on the 8 after those
     eng.set_profile(True)
     lat = []
-    for i in range(warm, min(warm + steps, warm + 8)):
+    for i in range(tb + 8, tb + 16):
         eng.process_batch(None, packed=batches[i])
         eng.synchronize()
         lat.append(eng.last_batch_ms())
@@ -76,7 +91,9 @@ def run_mode(cfg: dict, mode: str, steps: int, warm: int, pool_frac: float | Non
             "gpu_hit": ph["gpu_hit"], "total_hit": ph["total_hit"],
             "h2d_GBs": ph["h2d_bytes_per_step"] * steps / el / 1e9,
             "h2d_busy_frac": ph["h2d_bytes_per_step"] * steps / el / 55.5e9,
-            "evictions": ph["evictions"]}
+            "evictions": ph["evictions"],
+            "overlap": {"compute_hidden_frac": ov["compute_hidden_frac"], "h2d_busy_frac_cupti": ov["h2d_busy_frac"],
+                        "note": "CUPTI, 8 batches after the timed ones: fraction of kernel time with an H2D copy in flight"}}
 
 
 def main():
