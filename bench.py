@@ -23,7 +23,9 @@ Phases: A = device throughput (`value`, pre-packed requests, CUDA events);
 B = per-batch latency (p50/p99) with per-kernel CUDA-event timing of the
 attention launches (`roofline`) and the KV scatter/gather (`other_kernels`);
 C = end to end through the public API (`e2e`: Python request dicts -> C-ABI,
-pipelined submit / rankings read-back of every batch). Also reported:
+pipelined submit / rankings read-back of every batch); D (untimed) = 8 more
+batches under CUPTI for `overlap` (fraction of kernel time with an H2D copy in
+flight, H2D engine busy fraction). Also reported:
 `host_link` (H2D GB/s vs the measured pinned-copy peak), `control_plane`
 (planning cost; `--planner device` runs the GPU control plane), `cpu_baseline`
 (the unmodified reference on this box's host cores). Other BASELINE configs:
