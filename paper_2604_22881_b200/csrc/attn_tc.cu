@@ -693,9 +693,11 @@ __global__ void __launch_bounds__(384, 1)
             float o[16];
             tmem_ld16(o_col + c * PW, o);
             tmem_wait_ld();
+            // 64-B swizzled rows (the part map's SWIZZLE_64B): 16-B chunk k of row
+            // `lane` sits at chunk k ^ ((lane >> 1) & 3) — conflict-free stores
 #pragma unroll
             for (int k = 0; k < PW / 4; ++k)
-              *reinterpret_cast<float4*>(half + lane * PW + 4 * k) =
+              *reinterpret_cast<float4*>(half + lane * PW + 4 * (k ^ ((lane >> 1) & 3))) =
                   make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
             fence_async_smem();
             __syncwarp();
@@ -786,7 +788,7 @@ int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
 }
 
 // partial O slots [slots * 128 rows][D] fp32, box = 16 cols x 32 rows, no swizzle
-// (the attention epilogue's staged tiles; D = 128)
+// (the attention epilogue's staged tiles; D = 128; 64-B rows, 64-B swizzle)
 int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t D) {
   const cuuint64_t dims[2] = {D, rows};
   const cuuint64_t strides[1] = {cuuint64_t(D) * 4};
@@ -795,7 +797,7 @@ int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t 
   auto fn = encode_fn();
   if (!fn) return -1;
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(part_o), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
