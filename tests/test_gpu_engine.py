@@ -59,6 +59,31 @@ def test_tag_engine_bit_exact(case):
 
 
 @pytest.mark.parametrize("case", golden_cases("tag"), ids=lambda c: c["name"])
+def test_tag_engine_pipelined_bit_exact(case):
+    """The same traces with batches in flight (no per-batch read-back): onloads of
+    chunks persisted a few batches earlier, offload-slot reuse and the
+    ring-event rules (a batch leaving the 4-deep ring has its offload D2H
+    confirmed; waits only target batches still in the ring) must still move
+    every byte exactly — final control-plane state and a full conservation
+    read-back of pool + host store."""
+    ran = 0
+    for run in case["runs"]:
+        if run["mode"] == "recompute":
+            continue
+        eng = mtkv.Engine(_kv(case["kv"]), mode=run["mode"], backend="tag", batch_size=run["batch_size"])
+        for i, b in enumerate(batches(case["trace"], run["batch_size"])):
+            try:
+                eng.process_batch(b)
+            except mtkv.BatchRejected:
+                assert run["rejected"][i]
+        eng.drain()
+        assert eng.state() == run["final_state"]
+        eng.check_conservation()
+        ran += 1
+    assert ran > 0
+
+
+@pytest.mark.parametrize("case", golden_cases("tag"), ids=lambda c: c["name"])
 def test_device_planner_bit_exact(case):
     """GPU control plane (devctl.cu: batched lookup, LRU update, victim selection,
     LIFO page allocation) reproduces the reference's complete control-plane
