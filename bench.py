@@ -346,17 +346,27 @@ def run_b200(args, cfg):
     phase_c = _phase(e0, eng.report(), K, B)
 
     # ---- phase D (untimed): compute / transfer overlap of the next batches under CUPTI ----
-    overlap = None
+    overlap, cupti_copy = None, {}
     try:
         from torch.profiler import ProfilerActivity, profile
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import kernel_times
+        rd0 = eng.report()
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             for i in range(k1 + K, k1 + K + N_OVL):
                 eng.process_batch(None, packed=packed[i])
             eng.synchronize()
             torch.cuda.synchronize()
+        rd1 = eng.report()
         ov = kernel_times.overlap_stats(prof.events())
+        # the KV scatter / gather kernels' own start..end (CUPTI) over the same
+        # batches: CUDA-event brackets add the launch gap to these ~6-250 us kernels
+        for key, tag, chunks in (("scatter", "chunk_copy_kernel<true>", rd1["onload_chunks"] - rd0["onload_chunks"]),
+                                 ("gather", "chunk_copy_kernel<false>", rd1["offload_chunks"] - rd0["offload_chunks"])):
+            durs = [e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+                    for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and tag in e.name]
+            if durs and chunks:
+                cupti_copy[key] = (sum(durs), len(durs), chunks)
         overlap = {"compute_hidden_frac": ov["compute_hidden_frac"], "h2d_busy_frac": ov["h2d_busy_frac"],
                    "batches": N_OVL,
                    "note": "CUPTI timestamps: fraction of kernel time with an H2D copy in flight; H2D engine busy "
@@ -444,12 +454,21 @@ def run_b200(args, cfg):
     # bytes = read + write of every moved chunk ([L][2][chunk][d] bf16)
     cb = kv.chunk_bytes()
     kern = {}
-    for name, ms, ch, nl in (("chunk_scatter (onload: staging -> pages)", copy_stat[0], copy_stat[1], copy_stat[4]),
-                             ("chunk_gather (offload: pages -> slots)", copy_stat[2], copy_stat[3], copy_stat[5])):
+    for name, key, ms, ch, nl in (("chunk_scatter (onload: staging -> pages)", "scatter", copy_stat[0], copy_stat[1],
+                                   copy_stat[4]),
+                                  ("chunk_gather (offload: pages -> slots)", "gather", copy_stat[2], copy_stat[3],
+                                   copy_stat[5])):
         if ch:
             gbs = 2 * ch * cb / (ms / 1e3) / 1e9
             kern[name] = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                          "launches": nl, "avg_launch_us": ms / nl * 1e3, "bytes_per_launch": 2 * ch * cb / nl}
+                          "launches": nl, "avg_launch_us": ms / nl * 1e3, "bytes_per_launch": 2 * ch * cb / nl,
+                          "timing": "CUDA events around each launch (phase B)"}
+        if key in cupti_copy:
+            us, nl2, ch2 = cupti_copy[key]
+            g2 = 2 * ch2 * cb / (us / 1e6) / 1e9
+            kern.setdefault(name, {})["cupti"] = {
+                "achieved": g2, "frac": g2 / hbm_peak, "launches": nl2, "avg_launch_us": us / nl2,
+                "bytes_per_launch": 2 * ch2 * cb / nl2, "timing": "kernel start..end timestamps (CUPTI, phase D)"}
     if proj_stat[1]:
         # projection GEMM + fused paged K/V append: read activations (rows x d) and
         # W_in (d x 4d), write u | q (rows x 2d) and the K | V append (rows x 2d), bf16
