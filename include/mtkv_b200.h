@@ -206,6 +206,21 @@ uint32_t mtkv_lru_snapshot(const void* obj, int is_engine, uint32_t* out, uint32
 int mtkv_evict_user(void* obj, int is_engine, uint32_t user);                /* manager.cpp:141 */
 int mtkv_is_locked(const void* obj, int is_engine, uint32_t user);           /* manager.hpp:112 */
 uint64_t mtkv_get_total_cache_length(const void* obj, int is_engine, uint32_t user); /* :96 */
+/* Engine<B>::dump_page_map (sim.hpp:493): {"user":[page ids],...} over the known
+ * users in id order, byte-identical to the reference's string. malloc'd, free
+ * with mtkv_free. */
+char* mtkv_dump_page_map(const void* obj, int is_engine);
+/* Canonical binary image of the complete control-plane state (the fields of the
+ * reference driver's state dump: oracle/ref_driver.cpp dump_state), for
+ * bit-exact comparison at trace scale. Little-endian:
+ *   "MTKVST01", u64 n_users, then per known user in id order
+ *     u32 user, u32 locked, u64 total_len, device_len, persisted_len, last_access,
+ *     host_chunks, pending_offload, n_pages, u32 pages[n_pages];
+ *   u64 n_lru, u32 lru[n_lru] (most recent first);
+ *   u64 evictions, tail_tokens_lost, pages_allocated, occupied_pages, free_pages,
+ *     quota_in_flight; f64 clock.
+ * Writes min(size, cap) bytes to buf (may be NULL) and returns the full size. */
+int64_t mtkv_state_blob(const void* obj, int is_engine, uint8_t* buf, uint64_t cap);
 
 /* ---- workload (workload.cpp): identical RNG streams to the reference ---- */
 typedef struct {
@@ -250,6 +265,13 @@ int mtkv_op_paged_attention_batch(float* out, const void* q, const void* pool, c
                                   const uint32_t* page_off, const uint32_t* n_q, const uint64_t* p_pre,
                                   uint32_t n_req, uint32_t layer, const mtkv_kv_config* kv, uint32_t num_pages,
                                   uint32_t repeat, float* ms_per_launch, void* stream);
+/* Dense layer of the GR block (model.cpp:71 matmul; act = 1 applies the block's
+ * silu, model.cpp:174/:191): out[M x N] bf16 = act(a[M x K] . w[K x N]) with bf16
+ * operands (w row-major, the reference's layout) and fp32 accumulation, on the
+ * tcgen05 kernel when K and N are multiples of 64 (tc = 1: refuse other shapes),
+ * else the mma.sync kernel. a_rows_alloc = rows allocated behind `a` (>= M). */
+int mtkv_op_dense(void* out, const void* a, const void* w, uint32_t M, uint32_t N, uint32_t K,
+                  uint64_t a_rows_alloc, int act, int tc, void* stream);
 /* Host-only self-check of the attention work planner (attn_plan.cpp): plans a
  * batch (fresh history rows, candidates and cached prefix per request) for
  * `ctas` persistent CTAs and verifies every (request, head, query tile, key

@@ -351,9 +351,66 @@ class RefLib:
             raise OracleError(out["error"])
         return out
 
+    def run_blobs(self, req: dict, every: int = 64) -> dict:
+        """"run" with per-batch canonical state images (mtkv_state_blob layout)
+        hashed on the fly: returns the chained digest (see state_chain) sampled
+        every `every` batches, the rejected batch indices, the drained final
+        state's digest and the report."""
+        import hashlib
+        CB = C.CFUNCTYPE(None, C.c_uint64, C.POINTER(C.c_uint8), C.c_uint64, C.c_int)
+        if not hasattr(self.L, "_rb"):
+            self.L.mtkv_ref_run_blobs.restype = C.c_void_p
+            self.L.mtkv_ref_run_blobs.argtypes = [C.c_char_p, CB]
+            self.L._rb = True
+        chain = StateChain(every)
+        final = {}
+
+        def cb(i, data, n, rejected):
+            blob = C.string_at(data, n)
+            if i == 2**64 - 1:
+                final["digest"] = hashlib.sha256(blob).hexdigest()
+            else:
+                chain.add(blob, bool(rejected))
+
+        fn = CB(cb)
+        p = self.L.mtkv_ref_run_blobs(json.dumps(req).encode(), fn)
+        s = C.string_at(p).decode()
+        self.L.mtkv_ref_free(p)
+        out = json.loads(s)
+        if "error" in out:
+            raise OracleError(out["error"])
+        return dict(chain=chain.finish(), every=every, n_batches=chain.n, rejected=chain.rejected,
+                    final_digest=final["digest"], report=out["report"])
+
     def gen_trace(self, **gen) -> list:
         out = self.call({"cmd": "gen_trace", **gen})
         return [json.loads(line) for line in out["jsonl"].splitlines() if line.strip()]
+
+
+class StateChain:
+    """Chained digest of per-batch state images: c_0 = 32 zero bytes,
+    c_i = sha256(c_{i-1} || sha256(blob_i)); c_i is sampled at every `every`-th
+    batch and at the last one, so a divergence is located to an `every`-batch
+    window while the fixture stays small. Shared by the fixture generator and
+    the GPU replay tests (tests/test_gpu_scale.py)."""
+
+    def __init__(self, every: int = 64):
+        self.every, self.n, self.c = every, 0, bytes(32)
+        self.samples, self.rejected = [], []
+
+    def add(self, blob: bytes, rejected: bool = False) -> None:
+        import hashlib
+        self.c = hashlib.sha256(self.c + hashlib.sha256(blob).digest()).digest()
+        if rejected:
+            self.rejected.append(self.n)
+        self.n += 1
+        if self.n % self.every == 0:
+            self.samples.append(self.c.hex())
+
+    def finish(self) -> list:
+        if self.n % self.every:
+            self.samples.append(self.c.hex())
+        return self.samples
 
 
 def load_jsonl(path) -> list:

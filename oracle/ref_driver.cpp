@@ -140,8 +140,67 @@ json dump_state(Engine<B>& eng) {
 
 json report_json(const RunReport& r) { return json::parse(r.to_json()); }
 
+// The canonical binary state image of include/mtkv_b200.h mtkv_state_blob,
+// built here from the reference Engine's own accessors (independent encoder).
 template <class B>
-json run_engine(const json& req, const std::vector<Request>& trace) {
+void state_blob(Engine<B>& eng, std::vector<std::uint8_t>& b) {
+  b.clear();
+  auto put = [&b](const void* x, std::size_t n) {
+    const auto* c = static_cast<const std::uint8_t*>(x);
+    b.insert(b.end(), c, c + n);
+  };
+  auto u32 = [&put](std::uint32_t x) { put(&x, 4); };
+  auto u64 = [&put](std::uint64_t x) { put(&x, 8); };
+  put("MTKVST01", 8);
+  auto& mgr = eng.manager();
+  const std::vector<UserId> users = mgr.known_users();
+  u64(users.size());
+  for (UserId u : users) {
+    const SequenceState* s = mgr.find(u);
+    u32(u);
+    u32(s->locked ? 1 : 0);
+    u64(s->total_len);
+    u64(s->device_len);
+    u64(s->persisted_len);
+    u64(s->last_access);
+    u64(eng.host().chunk_count(u));
+    u64(eng.pending_offload_chunks(u));
+    const auto& pages = mgr.user_pages(u);
+    u64(pages.size());
+    for (PageId pg : pages) u32(pg);
+  }
+  const auto lru = mgr.lru().snapshot();
+  u64(lru.size());
+  for (UserId u : lru) u32(u);
+  u64(mgr.counters().evictions);
+  u64(mgr.counters().tail_tokens_lost);
+  u64(mgr.counters().pages_allocated);
+  u64(mgr.occupied_pages());
+  u64(eng.device().free_count());
+  u64(eng.quota().in_flight);
+  const double clk = eng.clock();
+  put(&clk, 8);
+}
+
+using BlobCb = void (*)(std::uint64_t batch, const std::uint8_t* data, std::uint64_t n, int rejected);
+
+// batch boundaries: explicit "batch_sizes" (a caller that batches a trace
+// unevenly, e.g. bench.py's prefill vs revisit batches), else batchify
+std::vector<std::vector<Request>> batches_of(const json& req, const std::vector<Request>& trace, std::uint32_t bs) {
+  if (!req.contains("batch_sizes")) return batchify(trace, bs);
+  std::vector<std::vector<Request>> out;
+  std::size_t at = 0;
+  for (std::size_t n : req["batch_sizes"].get<std::vector<std::size_t>>()) {
+    if (at + n > trace.size()) throw Error("batch_sizes exceed the trace");
+    out.emplace_back(trace.begin() + std::ptrdiff_t(at), trace.begin() + std::ptrdiff_t(at + n));
+    at += n;
+  }
+  if (at != trace.size()) throw Error("batch_sizes do not cover the trace");
+  return out;
+}
+
+template <class B>
+json run_engine(const json& req, const std::vector<Request>& trace, BlobCb blob_cb = nullptr) {
   KVConfig kv = kv_from(req.value("kv", json::object()));
   CostModel cost = cost_from(req.value("cost", json::object()));
   EngineOptions opts;
@@ -156,13 +215,15 @@ json run_engine(const json& req, const std::vector<Request>& trace) {
     opts.model = &params;
     opts.logit_sink = &logits;
   }
-  const bool dump = req.value("dump_state", true);
+  const bool dump = !blob_cb && req.value("dump_state", true);
+  std::vector<std::uint8_t> blob;
+  std::uint64_t bi = 0;
   const bool want_events = req.value("events", false);
   if (want_events) opts.event_sink = &events;
   Engine<B> eng(kv, cost, opts);
   json out;
   json batches = json::array();
-  for (const auto& batch : batchify(trace, opts.batch_size)) {
+  for (const auto& batch : batches_of(req, trace, opts.batch_size)) {
     json jb;
     std::size_t ev0 = events.size();
     try {
@@ -173,6 +234,11 @@ json run_engine(const json& req, const std::vector<Request>& trace) {
       jb["error"] = e.what();
     }
     if (dump) jb["state"] = dump_state(eng);
+    if (blob_cb) {
+      state_blob(eng, blob);
+      blob_cb(bi++, blob.data(), blob.size(), jb["rejected"].get<bool>() ? 1 : 0);
+      continue;  // per-batch results go through the callback only
+    }
     if (want_events) {
       json je = json::array();
       for (std::size_t i = ev0; i < events.size(); ++i)
@@ -190,7 +256,12 @@ json run_engine(const json& req, const std::vector<Request>& trace) {
       out["conservation"] = "ok";
     }
   }
-  out["final_state"] = dump_state(eng);
+  if (blob_cb) {
+    state_blob(eng, blob);
+    blob_cb(~std::uint64_t(0), blob.data(), blob.size(), 0);  // final state, after drain
+  } else {
+    out["final_state"] = dump_state(eng);
+  }
   out["report"] = report_json(eng.report());
   out["batches"] = std::move(batches);
   if constexpr (std::is_same_v<B, ValueBackend>) {
@@ -368,5 +439,25 @@ char* mtkv_ref_call(const char* request) {
 }
 
 void mtkv_ref_free(char* p) { std::free(p); }
+
+// "run" with the state image of every batch (and of the final, drained state,
+// batch = UINT64_MAX) handed to `cb` instead of the JSON state dumps: trace-scale
+// runs (thousands of batches, thousands of users) stay cheap to compare.
+char* mtkv_ref_run_blobs(const char* request, BlobCb cb) {
+  json out;
+  try {
+    json req = json::parse(request);
+    std::vector<Request> trace = trace_from(req["trace"]);
+    out = req.value("backend", std::string("tag")) == "value" ? run_engine<ValueBackend>(req, trace, cb)
+                                                              : run_engine<TagBackend>(req, trace, cb);
+  } catch (const std::exception& e) {
+    out = json::object();
+    out["error"] = e.what();
+  }
+  std::string s = out.dump();
+  char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return buf;
+}
 
 }  // extern "C"

@@ -134,9 +134,9 @@ EXPORTED_SYMBOLS = [
     "mtkv_engine_set_profile",
     "mtkv_report", "mtkv_last_plans", "mtkv_last_evictions", "mtkv_known_users", "mtkv_user_state",
     "mtkv_user_pages", "mtkv_lru_snapshot", "mtkv_evict_user", "mtkv_is_locked",
-    "mtkv_get_total_cache_length", "mtkv_gen_config_default", "mtkv_gen_config_preset",
+    "mtkv_get_total_cache_length", "mtkv_dump_page_map", "mtkv_state_blob", "mtkv_gen_config_default", "mtkv_gen_config_preset",
     "mtkv_generate_trace_jsonl", "mtkv_free", "mtkv_op_scatter_chunks", "mtkv_op_gather_chunks",
-    "mtkv_op_paged_attention", "mtkv_op_paged_attention_batch", "mtkv_attention_plan_check",
+    "mtkv_op_paged_attention", "mtkv_op_paged_attention_batch", "mtkv_op_dense", "mtkv_attention_plan_check",
 ]
 
 _lib = None
@@ -195,12 +195,15 @@ def lib():
         "mtkv_evict_user": (C.c_int, [vp, C.c_int, u32]),
         "mtkv_is_locked": (C.c_int, [vp, C.c_int, u32]),
         "mtkv_get_total_cache_length": (u64, [vp, C.c_int, u32]),
+        "mtkv_dump_page_map": (vp, [vp, C.c_int]),
+        "mtkv_state_blob": (C.c_int64, [vp, C.c_int, C.POINTER(C.c_uint8), u64]),
         "mtkv_gen_config_default": (None, [C.POINTER(_GenCfg)]),
         "mtkv_gen_config_preset": (C.c_int, [C.c_char_p, C.POINTER(_GenCfg)]),
         "mtkv_generate_trace_jsonl": (vp, [C.POINTER(_GenCfg)]),
         "mtkv_free": (None, [vp]),
         "mtkv_op_scatter_chunks": (C.c_int, [vp, vp, vp, u32, C.POINTER(_KV), u32, vp]),
         "mtkv_op_gather_chunks": (C.c_int, [vp, vp, vp, u32, C.POINTER(_KV), u32, vp]),
+        "mtkv_op_dense": (C.c_int, [vp, vp, vp, u32, u32, u32, u64, C.c_int, C.c_int, vp]),
         "mtkv_op_paged_attention": (C.c_int, [vp, vp, vp, vp, u32, u64, u64, u32, C.POINTER(_KV),
                                               u32, vp]),
         "mtkv_attention_plan_check": (C.c_int, [u32, u32p, u32p, C.POINTER(C.c_uint64), u32, u32, u32, u32, C.c_int,
@@ -433,6 +436,21 @@ class _ManagerView:
 
     def get_total_cache_length(self, user: int) -> int:
         return int(lib().mtkv_get_total_cache_length(self._h, self._is_engine, user))
+
+    def dump_page_map(self) -> str:
+        """Engine<B>::dump_page_map (sim.hpp:493): same JSON text as the reference."""
+        p = lib().mtkv_dump_page_map(self._h, self._is_engine)
+        try:
+            return C.string_at(p).decode()
+        finally:
+            lib().mtkv_free(p)
+
+    def state_blob(self) -> bytes:
+        """Canonical binary image of the control-plane state (mtkv_state_blob)."""
+        n = lib().mtkv_state_blob(self._h, self._is_engine, None, 0)
+        buf = (C.c_uint8 * n)()
+        lib().mtkv_state_blob(self._h, self._is_engine, buf, n)
+        return bytes(buf)
 
     def state(self) -> dict:
         """Full control-plane state, same schema as the reference driver's dump."""

@@ -810,11 +810,9 @@ int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g
 template <int D, bool TR, int POLY>
 static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
                        const AttnArgs& a, cudaStream_t s) {
-  static bool set = false;
-  if (!set) {
+  static DeviceOnce once;
+  if (once.first())
     cudaFuncSetAttribute(attn_tc_kernel<D, TR, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TcCfg<D>::SMEM));
-    set = true;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.n_items);
   cfg.blockDim = dim3(384);

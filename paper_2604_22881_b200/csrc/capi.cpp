@@ -343,6 +343,72 @@ uint64_t mtkv_get_total_cache_length(const void* obj, int is_engine, uint32_t us
   return u->device_len > u->persisted_len ? u->device_len : u->persisted_len;
 }
 
+char* mtkv_dump_page_map(const void* obj, int is_engine) {
+  const Planner* p = planner_of(obj, is_engine);
+  std::string s = "{";
+  bool first = true;
+  for (uint32_t u : p->known_users()) {
+    if (!first) s += ",";
+    first = false;
+    s += "\"" + std::to_string(u) + "\":[";
+    const UserRec* r = p->find(u);
+    if (r && r->has_pages)
+      for (size_t i = 0; i < r->pages.size(); ++i) {
+        if (i) s += ",";
+        s += std::to_string(r->pages[i]);
+      }
+    s += "]";
+  }
+  s += "}";
+  char* out = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return out;
+}
+
+int64_t mtkv_state_blob(const void* obj, int is_engine, uint8_t* buf, uint64_t cap) {
+  const Planner* p = planner_of(obj, is_engine);
+  std::vector<uint8_t> b;
+  b.reserve(1 << 16);
+  auto put = [&b](const void* x, size_t n) {
+    const uint8_t* c = static_cast<const uint8_t*>(x);
+    b.insert(b.end(), c, c + n);
+  };
+  auto u32 = [&put](uint32_t x) { put(&x, 4); };
+  auto u64 = [&put](uint64_t x) { put(&x, 8); };
+  put("MTKVST01", 8);
+  const std::vector<uint32_t> users = p->known_users();
+  u64(users.size());
+  for (uint32_t id : users) {
+    const UserRec* u = p->find(id);
+    u32(id);
+    u32(u->locked ? 1 : 0);
+    u64(u->total_len);
+    u64(u->device_len);
+    u64(u->persisted_len);
+    u64(u->last_access);
+    u64(u->host_chunks.size());
+    u64(u->pending);
+    const size_t np = u->has_pages ? u->pages.size() : 0;
+    u64(np);
+    if (np) put(u->pages.data(), np * 4);
+  }
+  const std::vector<uint32_t> lru = p->lru_snapshot();
+  u64(lru.size());
+  if (!lru.empty()) put(lru.data(), lru.size() * 4);
+  mtkv_run_report r;
+  if (is_engine) static_cast<const mtkv_engine*>(obj)->e.report(r);
+  else p->report(r);
+  u64(r.evictions);
+  u64(r.tail_tokens_lost);
+  u64(r.pages_allocated);
+  u64(r.occupied_pages);
+  u64(r.free_pages);
+  u64(r.quota_in_flight);
+  put(&r.clock, 8);
+  if (buf) std::memcpy(buf, b.data(), std::min<uint64_t>(cap, b.size()));
+  return int64_t(b.size());
+}
+
 // --------------------------------------------------------------- workload --
 void mtkv_gen_config_default(mtkv_gen_config* g) {
   *g = mtkv_gen_config{100, 2000, 0, 9.0, 1.5, 1.3, 1000.0, 6375.0, 1, 20000, 0, 5, 0, 42};

@@ -40,6 +40,7 @@ struct Args {
   uint32_t* ids;
   uint32_t device_pages, page_size, chunk_size, max_users, max_pages, hash_mask;
   uint32_t hier;
+  uint64_t staging_tokens;  // onload staging capacity (KVConfig::onload_pages * page_size)
 };
 
 __device__ __forceinline__ uint32_t hash_u32(uint32_t x) {
@@ -61,7 +62,7 @@ struct Smem {
   uint32_t vnp[kMaxVictims];    // pages a victim frees
   uint32_t vpos[kMaxVictims];   // stack position its first page is pushed to
   uint32_t vreq[kMaxVictims];   // request whose ensure_free evicted it
-  uint32_t min_pos, max_pos, final_top, scratch_total;
+  uint32_t min_pos, max_pos, final_top, scratch_total, old_slots;
 };
 
 __device__ uint64_t block_sum64(uint64_t v, Smem& sm) {
@@ -74,6 +75,30 @@ __device__ uint64_t block_sum64(uint64_t v, Smem& sm) {
   for (int i = 0; i < kThreads / 32; ++i) t += sm.red64[i];
   __syncthreads();
   return t;
+}
+
+// A batch the device tables cannot hold (CTL_CAPACITY) or the staging buffer
+// cannot onload (CTL_STAGING) fails before any state changes except step 1's
+// new users: remove their hash entries again. With linear probing this is
+// exact because every key inserted by this batch is removed (older keys never
+// probed through those positions: they were empty when the older keys went in).
+__device__ void rollback_inserts(const Args& a, const uint32_t* r_slot, uint32_t old_slots, int32_t fail) {
+  const State& S = a.s;
+  for (uint32_t i = 0; i < a.n; ++i) {
+    if (r_slot[i] < old_slots || r_slot[i] == kEmpty) continue;
+    const uint32_t user = a.reqs[i].user;
+    for (uint32_t h = hash_u32(user) & a.hash_mask;; h = (h + 1) & a.hash_mask) {
+      const uint32_t k = S.keys[h];
+      if (k == kEmpty) break;
+      if (k == user) { S.keys[h] = kEmpty; break; }
+    }
+  }
+  S.g->n_slots = old_slots;
+  CtlHdr h{};
+  h.fail = fail;
+  h.fail_at = 0;
+  h.n_slots = old_slots;
+  *a.hdr = h;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
@@ -106,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     sm.fail = CTL_OK;
     sm.fail_at = a.n;
     sm.n_vict = 0;
+    sm.old_slots = G.n_slots;
   }
   __syncthreads();
 
@@ -156,14 +182,14 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
         n_slots += __popc(leaders);
         __threadfence_block();
       }
-      if (act) r_slot[i] = uint32_t(slot);
+      if (act) r_slot[i] = slot < 0 ? kEmpty : uint32_t(slot);
       __syncwarp();
     }
     if (lane == 0) G.n_slots = min(n_slots, a.max_users);
   }
   __syncthreads();
   if (sm.fail == CTL_CAPACITY) {
-    if (tid == 0) { a.hdr->fail = CTL_CAPACITY; a.hdr->fail_at = 0; }
+    if (tid == 0) rollback_inserts(a, r_slot, sm.old_slots, CTL_CAPACITY);
     return;
   }
   const uint32_t epoch = G.epoch + 1;
@@ -216,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
       const uint64_t scratch = div_up(nc, a.page_size);
       batch_need += grow + scratch;
       if (batch_need > a.device_pages) { fail = CTL_REJECT_PAGES; fail_at = i; break; }
+      if (have + grow > a.max_pages) { fail = CTL_CAPACITY; fail_at = i; break; }  // page-table row full
       r_grow[i] = uint32_t(grow);
       r_scr[i] = uint32_t(scratch);
       r_cum[i] = batch_need;
@@ -229,6 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     sm.fail_at = fail_at;
   }
   __syncthreads();
+  if (sm.fail == CTL_CAPACITY) {  // nothing but the step-1 inserts has changed yet
+    if (tid == 0) rollback_inserts(a, r_slot, sm.old_slots, CTL_CAPACITY);
+    return;
+  }
   // ---- 4. eviction victims: oldest stamps among in-list, unlocked, not-in-batch users ----
   const uint32_t n_ok = sm.fail_at;  // requests whose allocation is attempted
   const uint64_t free0 = G.top;
@@ -253,11 +284,20 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     } else {
       const uint64_t cum = n_ok ? r_cum[n_ok - 1] : 0;
       sm.need = cum > free0 ? cum - free0 : 0;
+      if (sm.fail == CTL_OK && a.staging_tokens) {  // the onload staging check (sim.hpp:371) comes
+        uint64_t tok = 0;                           // after a successful prepare_metadata
+        for (uint32_t i = 0; i < n_ok; ++i) tok += uint64_t(a.plans[i].onload_chunks) * a.chunk_size;
+        if (tok > a.staging_tokens) sm.fail = CTL_STAGING;
+      }
     }
     sm.prefix = 0;
     sm.prefix_bits = 0;
   }
   __syncthreads();
+  if (sm.fail == CTL_STAGING) {
+    if (tid == 0) rollback_inserts(a, r_slot, sm.old_slots, CTL_STAGING);
+    return;
+  }
   const uint64_t need = sm.need;
   if (need > 0) {
     uint64_t thresh = ~uint64_t(0);
@@ -322,8 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
     }
     __syncthreads();
     const uint32_t nv = sm.n_vict;
-    if (nv > kMaxVictims) {
-      if (tid == 0) { a.hdr->fail = CTL_CAPACITY; a.hdr->fail_at = 0; }
+    if (nv > kMaxVictims) {  // victims are only selected so far: undo the inserts and report
+      if (tid == 0) rollback_inserts(a, r_slot, sm.old_slots, CTL_CAPACITY);
       return;
     }
     uint32_t np2 = 1;
@@ -488,7 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1) ctl_prepare_kernel(Args a) {
 }  // namespace
 
 int DevCtl::init(uint32_t device_pages, uint32_t page_size, uint32_t chunk_size, bool hier, uint32_t max_users,
-                 uint32_t max_pages_per_user, std::string& err) {
+                 uint32_t max_pages_per_user, uint64_t staging_tokens, std::string& err) {
+  staging_tokens_ = staging_tokens;
   device_pages_ = device_pages;
   page_size_ = page_size;
   chunk_size_ = chunk_size;
@@ -589,6 +630,7 @@ int DevCtl::prepare(const CtlReq* reqs, uint32_t n, const std::vector<CtlUpd>& u
   a.max_pages = max_pages_;
   a.hash_mask = hash_cap_ - 1;
   a.hier = hier_ ? 1 : 0;
+  a.staging_tokens = staging_tokens_;
   cudaEventRecord(ev0_, st_);
   ctl_prepare_kernel<<<1, kThreads, smem, st_>>>(a);
   cudaEventRecord(ev1_, st_);
@@ -610,8 +652,12 @@ int DevCtl::prepare(const CtlReq* reqs, uint32_t n, const std::vector<CtlUpd>& u
   float ms = 0;
   cudaEventElapsedTime(&ms, ev0_, ev1_);
   last_ms_ = ms;
-  if (hdr_.fail == CTL_CAPACITY) {
-    err = "device planner: capacity exceeded (max_users / max_pages_per_user / victims per batch)";
+  if (hdr_.fail == CTL_CAPACITY) {  // rolled back on the device: the tables are as before the batch
+    err = "device planner: capacity exceeded (max_users / max_user_pages / 4096 victims per batch)";
+    return -1;
+  }
+  if (hdr_.fail == CTL_STAGING) {
+    err = "onload buffer: batch exceeds staging capacity";
     return -1;
   }
   return 0;

@@ -49,7 +49,7 @@ struct CtlEvict {
   uint32_t slot, user, freed_pages, pad;
   uint64_t tail_lost;
 };
-enum CtlFail : int32_t { CTL_OK = 0, CTL_REJECT_PAGES = 1, CTL_REJECT_VICTIMS = 2, CTL_BAD_REQUEST = 3, CTL_CAPACITY = 4 };
+enum CtlFail : int32_t { CTL_OK = 0, CTL_REJECT_PAGES = 1, CTL_REJECT_VICTIMS = 2, CTL_BAD_REQUEST = 3, CTL_CAPACITY = 4, CTL_STAGING = 5 };
 struct CtlHdr {
   int32_t fail;      // CtlFail
   int32_t fail_at;   // request index of the failure (touched, not allocated)
@@ -61,7 +61,7 @@ class DevCtl {
  public:
   // page_size/chunk_size/device_pages: KVConfig; hier: host tier enabled
   int init(uint32_t device_pages, uint32_t page_size, uint32_t chunk_size, bool hier, uint32_t max_users,
-           uint32_t max_pages_per_user, std::string& err);
+           uint32_t max_pages_per_user, uint64_t staging_tokens, std::string& err);
   ~DevCtl();
   // One batch: updates, then prepare + commit + append + scratch release on the
   // device; blocks until the decisions are back on the host.
@@ -76,6 +76,7 @@ class DevCtl {
  private:
   uint32_t device_pages_ = 0, page_size_ = 0, chunk_size_ = 0, max_users_ = 0, max_pages_ = 0, hash_cap_ = 0;
   bool hier_ = false;
+  uint64_t staging_tokens_ = 0;
   cudaStream_t st_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   void* state_ = nullptr;  // device tables

@@ -26,10 +26,22 @@ namespace mtkv_b200 {
     }                                                           \
   } while (0)
 
-int DevBuf::ensure(size_t need) {
+int DevBuf::ensure(size_t need, cudaStream_t s) {
   if (need <= bytes) return 0;
   size_t nb = std::max(need, bytes * 2);
   nb = (nb + 255) & ~size_t(255);
+  if (s) {
+    // stream-ordered: the old buffer is freed after the work already queued on
+    // `s` (its only user) and the new one is valid for work queued after this
+    // call, so a workspace growing mid-serve stalls nothing
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    bytes = 0;
+    if (cudaMallocAsync(&p, nb, s) != cudaSuccess) return -1;
+    async = true;
+    bytes = nb;
+    return 0;
+  }
   if (p) {
     cudaDeviceSynchronize();
     cudaFree(p);
@@ -42,7 +54,7 @@ int DevBuf::ensure(size_t need) {
 }
 
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) async ? cudaFreeAsync(p, 0) : cudaFree(p);
   p = nullptr;
   bytes = 0;
 }
@@ -241,7 +253,7 @@ int Engine::init(std::string& err) {
       return MTKV_ERROR;
     }
     if (ctl_.init(kv_.device_pages, kv_.page_size, kv_.chunk_size, opt_.mode == MTKV_MODE_HIERARCHICAL, max_users,
-                  max_pages, err))
+                  max_pages, uint64_t(kv_.onload_pages) * kv_.page_size, err))
       return MTKV_ERROR;
     planner.set_device_ctl(&ctl_);
   }
@@ -344,8 +356,29 @@ int Engine::gemm(const GemmArgs& a, uint64_t a_rows_alloc, std::string& err) {
   return MTKV_OK;
 }
 
+// Value backend: the payload is validated before the planner touches any state
+// (a batch that fails here leaves the engine exactly as it was). The messages
+// are the reference model's (model.cpp:159, :162; manager.cpp:103).
+int Engine::validate_payload(const mtkv_request* reqs, uint32_t n, std::string& err) const {
+  const uint32_t V = opt_.model.vocab;
+  for (uint32_t i = 0; i < n; ++i) {
+    const mtkv_request& r = reqs[i];
+    if (r.candidate_count < 1) { err = "request: need at least one candidate"; return MTKV_ERROR; }
+    if ((r.new_token_count && !r.new_tokens) || !r.candidates) {
+      err = "value mode: trace must carry explicit token ids";
+      return MTKV_ERROR;
+    }
+    for (uint32_t j = 0; j < r.new_token_count; ++j)
+      if (r.new_tokens[j] >= V) { err = "forward: token id out of vocabulary"; return MTKV_ERROR; }
+    for (uint32_t j = 0; j < r.candidate_count; ++j)
+      if (r.candidates[j] >= V) { err = "forward: token id out of vocabulary"; return MTKV_ERROR; }
+  }
+  return MTKV_OK;
+}
+
 int Engine::process_batch(const mtkv_request* reqs, uint32_t n, std::string& err) {
   CK(cudaSetDevice(opt_.device));
+  if (value_ && validate_payload(reqs, n, err)) return MTKV_ERROR;
   BatchWork w;
   const auto t0 = std::chrono::steady_clock::now();
   planner.plan_batch(reqs, n, w);
@@ -394,7 +427,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     }
     if (next > g_.num_pages) {
       g_.num_pages = std::max<uint32_t>(next, g_.num_pages * 2);
-      if (pool_.ensure(size_t(g_.L) * g_.num_pages * 2 * S * d * sizeof(__nv_bfloat16))) {
+      if (pool_.ensure(size_t(g_.L) * g_.num_pages * 2 * S * d * sizeof(__nv_bfloat16), comp_)) {
         err = "engine: cannot grow the transient page pool";
         return MTKV_ERROR;
       }
@@ -623,10 +656,12 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   attn_launches_last_ = 0;
   if (value_) {
     const size_t rb = size_t(rows) * d * sizeof(__nv_bfloat16);
-    if (x_.ensure(rb) || x2_.ensure(rb) || u_.ensure(rb) || q_.ensure(rb) || mid_.ensure(rb) ||
-        part_o_.ensure(size_t(plan_.n_slots) * bq * g_.D * sizeof(float)) ||
-        part_lse_.ensure(size_t(plan_.n_slots) * bq * sizeof(float)) ||
-        logits_.ensure(size_t(n) * V * sizeof(float)) || scores_.ensure(size_t(ncand_total) * sizeof(float))) {
+    // comp-only workspaces: stream-ordered growth (no device synchronisation)
+    if (x_.ensure(rb, comp_) || x2_.ensure(rb, comp_) || u_.ensure(rb, comp_) || q_.ensure(rb, comp_) ||
+        mid_.ensure(rb, comp_) || part_o_.ensure(size_t(plan_.n_slots) * bq * g_.D * sizeof(float), comp_) ||
+        part_lse_.ensure(size_t(plan_.n_slots) * bq * sizeof(float), comp_) ||
+        logits_.ensure(size_t(n) * V * sizeof(float), comp_) ||
+        scores_.ensure(size_t(ncand_total) * sizeof(float), comp_)) {
       err = "engine: workspace alloc";
       return MTKV_ERROR;
     }

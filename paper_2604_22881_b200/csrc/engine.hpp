@@ -31,7 +31,10 @@ constexpr int kRing = 4;  // batches in flight on the device
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
-  int ensure(size_t need);  // grows (device-synchronising) when needed
+  bool async = false;        // allocated stream-ordered
+  // grows when needed: stream-ordered on `s` when the buffer is only used on
+  // that stream, else device-synchronising
+  int ensure(size_t need, cudaStream_t s = nullptr);
   void release();
 };
 
@@ -75,6 +78,7 @@ class Engine {
 
  private:
   int enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, std::string& err);
+  int validate_payload(const mtkv_request* reqs, uint32_t n, std::string& err) const;
   int host_chunk(uint64_t id, uint32_t user, uint32_t index, std::string& err);  // pinned storage
   char* take_slab();
   void slab_refill_loop();

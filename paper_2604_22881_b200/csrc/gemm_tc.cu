@@ -15,7 +15,7 @@
 #include <cstdio>
 #include <cudaTypedefs.h>
 
-#include <vector>
+#include <deque>
 
 #include "kernels.cuh"
 
@@ -257,11 +257,8 @@ bool gemm_tc_supported(const GemmArgs& a) {
 template <int BN>
 static void launch_bn(const CUtensorMap& am, const CUtensorMap& wm, const GemmArgs& a, cudaStream_t s) {
   constexpr size_t smem = 1024 + NSTG * (BM * BK * 2 + BK * BN * 2) + 128;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    set = true;
-  }
+  static DeviceOnce once;  // the attribute is per device
+  if (once.first()) cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.N / BN, (a.M + BM - 1) / BM);
   cfg.blockDim = dim3(128);
@@ -285,32 +282,34 @@ struct MapKey {
     return p == o.p && cols == o.cols && rows == o.rows && bc == o.bc && br == o.br;
   }
 };
-static const CUtensorMap* cached_map(const void* base, uint64_t cols, uint64_t rows, uint32_t bc, uint32_t br) {
+// The map is returned by value: an Entry lives in a std::deque only while it
+// is looked up, and a later lookup may evict (or, with a vector, move) it.
+static bool cached_map(CUtensorMap* out, const void* base, uint64_t cols, uint64_t rows, uint32_t bc, uint32_t br) {
   struct Entry {
     MapKey k;
     alignas(64) CUtensorMap m;
   };
-  static thread_local std::vector<Entry> cache;
+  static thread_local std::deque<Entry> cache;
   const MapKey k{base, cols, rows, bc, br};
   for (const Entry& e : cache)
-    if (e.k == k) return &e.m;
-  if (cache.size() >= 64) cache.erase(cache.begin());
-  cache.emplace_back();
-  cache.back().k = k;
-  if (!encode(&cache.back().m, base, cols, rows, bc, br)) {
-    cache.pop_back();
-    return nullptr;
-  }
-  return &cache.back().m;
+    if (e.k == k) {
+      *out = e.m;
+      return true;
+    }
+  Entry e;
+  e.k = k;
+  if (!encode(&e.m, base, cols, rows, bc, br)) return false;
+  if (cache.size() >= 64) cache.pop_front();
+  cache.push_back(e);
+  *out = e.m;
+  return true;
 }
 
 // A: [M x K] activations (rows padded by TMA zero fill), W: [K x N] row-major weights
 int launch_gemm_tc(const GemmArgs& a, uint64_t a_rows_alloc, cudaStream_t s) {
   if (a.M <= 0) return 0;
-  const CUtensorMap* amp = cached_map(a.A, a.K, a_rows_alloc, BK, BM);
-  const CUtensorMap* wmp = cached_map(a.B, a.N, a.K, 64, BK);
-  if (!amp || !wmp) return -1;
-  const CUtensorMap am = *amp, wm = *wmp;
+  alignas(64) CUtensorMap am, wm;
+  if (!cached_map(&am, a.A, a.K, a_rows_alloc, BK, BM) || !cached_map(&wm, a.B, a.N, a.K, 64, BK)) return -1;
   // wide N (projection, 4d): 128-column tiles (measured 16.5 us vs 18.7 us with
   // 64-column tiles, and a 415 vs 439 us layer-stack span against 256-column
   // tiles at 2 CTAs per SM); narrow N (MLP, d): 64-column tiles

@@ -426,11 +426,8 @@ __global__ void __launch_bounds__(NW * 32) attn_kernel(AttnArgs a) {
 template <int DP, bool VEC, int NW>
 static void launch_attn_cfg(const AttnArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)(NW * 16 + 4 * ABK) * (DP + 8) * sizeof(__nv_bfloat16);
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(attn_kernel<DP, VEC, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = true;
-  }
+  static DeviceOnce once;
+  if (once.first()) cudaFuncSetAttribute(attn_kernel<DP, VEC, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   attn_kernel<DP, VEC, NW><<<a.n_items, NW * 32, smem, s>>>(a);
 }
 

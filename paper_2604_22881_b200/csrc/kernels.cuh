@@ -6,6 +6,8 @@
 // onload staging slots use [L][2][chunk_size][H*D] bf16, so one chunk is one
 // contiguous copy-engine transfer.
 #pragma once
+
+#include <atomic>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -166,6 +168,19 @@ int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t 
 void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
                          const AttnArgs& a, cudaStream_t s);
 int num_sms();
+
+// once per CUDA device (kernel attributes such as the dynamic smem opt-in are
+// per device; a process may drive several GPUs)
+struct DeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::atomic<bool> done[kMaxDev] = {};
+  bool first() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) return true;
+    return !done[dev].exchange(true);
+  }
+};
 }  // namespace mtkv_b200
 
 // ---- host-side attention planning (attn_plan.cpp) ----

@@ -254,3 +254,33 @@ int mtkv_op_paged_attention_batch(float* out, const void* q, const void* pool, c
 }
 
 }  // extern "C"
+
+// Dense layer of the GR block (model.cpp:71 matmul, with the silu of :174/:191
+// when act = 1): out[M x N] bf16 = act(a[M x K] . w[K x N]), fp32 accumulation.
+// The tcgen05 kernel runs whenever it covers the shape (K, N multiples of 64),
+// the mma.sync kernel otherwise; tc = 1 refuses shapes the tcgen05 kernel does
+// not cover instead of falling back. a_rows_alloc: rows allocated behind `a`.
+extern "C" int mtkv_op_dense(void* out, const void* a, const void* w, uint32_t M, uint32_t N, uint32_t K,
+                             uint64_t a_rows_alloc, int act, int tc, void* stream) {
+  GemmArgs g{};
+  g.A = static_cast<const __nv_bfloat16*>(a);
+  g.B = static_cast<const __nv_bfloat16*>(w);
+  g.M = int(M);
+  g.N = int(N);
+  g.K = int(K);
+  g.epi = act ? Epi::SiluBf16 : Epi::Bf16;
+  g.out = out;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (gemm_tc_supported(g)) {
+    if (launch_gemm_tc(g, a_rows_alloc < M ? M : a_rows_alloc, s)) {
+      set_last_error("dense: cuTensorMapEncodeTiled failed");
+      return MTKV_ERROR;
+    }
+  } else if (tc) {
+    set_last_error("dense: shape not covered by the tcgen05 kernel (K and N must be multiples of 64)");
+    return MTKV_ERROR;
+  } else {
+    launch_gemm(g, s);
+  }
+  return finish(cudaSuccess);
+}

@@ -404,3 +404,82 @@ def test_scatter_gather_round_trip_bit_exact():
     for c in range(n_chunks):
         for p in range(ppc):
             assert torch.equal(pool[:, pl[c, p]], staging[c, :, :, p * S:(p + 1) * S])
+
+
+def test_dense_op_many_operand_buffers_vs_torch():
+    """The tcgen05 GEMM's tensor-map cache (64 entries) under more than 64
+    distinct operand buffers, revisited after eviction: every result must use
+    its own operands (regression: a cached map pointer into a growing vector)."""
+    s = torch.cuda.current_stream().cuda_stream
+    shapes = [(1, 64, 64), (77, 128, 256), (128, 256, 256), (300, 1024, 256), (513, 256, 512), (64, 2048, 512)]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    bufs = []
+    for i in range(80):
+        M, N, K = shapes[i % len(shapes)]
+        a = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+        w = (torch.randn(K, N, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+        bufs.append((a, w, i % 2))
+    worst = 0.0
+    for rep in range(2):
+        for a, w, act in bufs:
+            M, K = a.shape
+            N = w.shape[1]
+            out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            assert mtkv.lib().mtkv_op_dense(out.data_ptr(), a.data_ptr(), w.data_ptr(), M, N, K, M, act, 1, s) == 0, \
+                mtkv._err()
+            ref = a.float() @ w.float()
+            if act:
+                ref = ref * torch.sigmoid(ref)
+            err = ((out.float() - ref).abs().max() / ref.abs().max()).item()
+            worst = max(worst, err)
+            assert err <= 1e-2, (M, N, K, act, err)
+    print(f"dense op: 160 launches over 80 operand pairs, worst rel err {worst:.2e}")
+
+
+def test_device_planner_capacity_error_rolls_back():
+    """A batch that overflows the device planner's page table (max_user_pages)
+    fails with an error and leaves the device tables, the host mirror and the
+    data exactly as before: later batches stay bit-identical to a host-planner
+    engine that never saw the failing batch."""
+    kv = _kv(dict(num_layers=2, num_heads=1, head_dim=4, page_size=8, chunk_size=16, device_pages=400,
+                  offload_quota=256))
+    dev = mtkv.Engine(kv, mode="hierarchical", backend="tag", planner="device", max_users=64, max_user_pages=6)
+    host = mtkv.Engine(kv, mode="hierarchical", backend="tag")
+    ok1 = [{"ts": 0, "user": 1, "dn": 20, "nc": 1}, {"ts": 1, "user": 2, "dn": 30, "nc": 1}]
+    too_big = [{"ts": 2, "user": 3, "dn": 10, "nc": 1}, {"ts": 3, "user": 1, "dn": 60, "nc": 1}]  # user 1 -> 10 pages
+    ok2 = [{"ts": 4, "user": 2, "dn": 8, "nc": 1}, {"ts": 5, "user": 4, "dn": 16, "nc": 1}]
+    for e in (dev, host):
+        e.process_batch(ok1)
+    before = dev.state_blob()
+    with pytest.raises(mtkv.Error, match="capacity"):
+        dev.process_batch(too_big)
+    assert dev.state_blob() == before
+    for e in (dev, host):
+        e.process_batch(ok2)
+    assert dev.state_blob() == host.state_blob()
+    dev.drain()
+    host.drain()
+    assert dev.state_blob() == host.state_blob()
+    dev.check_conservation()
+
+
+def test_value_payload_rejected_before_any_state_change():
+    """Value backend: token / candidate ids out of the vocabulary, a missing
+    token array or no candidates fail with the reference's messages
+    (model.cpp:159, manager.cpp:103) before the planner changes anything."""
+    case = [c for c in golden_cases("value") if c["name"] == "value10"][0]
+    m = mtkv.ModelConfig(**case["model"])
+    eng = mtkv.Engine(_kv(case["kv"]), mode="hierarchical", backend="value", batch_size=2, model=m)
+    eng.process_batch(case["trace"][:2])
+    before = eng.state_blob()
+    V = case["model"]["vocab"]
+    good = {"ts": 9, "user": 3, "dn": 4, "nc": 2, "tokens": [1, 2, 3, 4], "cands": [1, 2]}
+    for bad, msg in [({**good, "tokens": [1, 2, V, 4]}, "out of vocabulary"),
+                     ({**good, "cands": [1, V + 5]}, "out of vocabulary"),
+                     ({"ts": 9, "user": 3, "dn": 4, "nc": 2, "cands": [1, 2]}, "explicit token ids"),
+                     ({**good, "nc": 0, "cands": []}, "at least one candidate")]:
+        with pytest.raises(mtkv.Error, match=msg):
+            eng.process_batch([good, bad])
+        assert eng.state_blob() == before
+    eng.process_batch([good])
+    assert eng.state_blob() != before

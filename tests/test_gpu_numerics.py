@@ -1,0 +1,171 @@
+"""Numerics bars that can fail (B200):
+
+* attention op: per (query row, head) relative error ||out - ref||_inf /
+  ||ref||_inf <= ATTN_REL against a torch fp32 reference on the same bf16
+  inputs, with PEAKED softmax (scores std ~3, so one or a few keys dominate each
+  row) and POISONED slots: page padding past the last key, every page not in
+  the request's list, and planted huge keys inside the fresh rows (legal for
+  later rows, masked for earlier ones). A dropped key tile, a mask off by one
+  or a stale page read moves the output by far more than the bar; the test also
+  proves that on the reference side (the bar rejects the reference with one key
+  tile dropped and with the causal mask shifted by one).
+* value engine at the configs[1] model dims (L=4, d=256, H=2, D=128, 4K-token
+  prefixes, vocab 4096): 32 users through prefill -> eviction -> host onload
+  (+ recomputed lost tail) -> revisit, in all three modes, every request's
+  logits against the fp64 restatement of the reference model
+  (tests/ref_model.py, pinned to the reference): per request max|dlogit| <=
+  LOGIT_REL x max|ref logit|; and the modes against each other <= MODE_REL
+  (the reference's acceptance criterion 2, tests/acceptance.cpp:104, requires
+  mode-invariant logits; here within bf16 storage / fp32 accumulation).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_22881_b200 as mtkv
+from oracle.oracle import ModelParams
+from tests.ref_model import RefModel, RefServer
+
+pytestmark = pytest.mark.gpu
+
+ATTN_REL = 1e-2
+LOGIT_REL = 0.03
+MODE_REL = 1e-2
+POISON_K, POISON_V = 30.0, 1000.0
+
+
+def _kv(d):
+    return mtkv.KVConfig(**{**mtkv.KVConfig().__dict__, **d})
+
+
+def _ref_attention(q, K, V, n_keys, p_pre, H, D, drop_tile=None, mask_shift=0):
+    n_q = q.shape[0]
+    out = torch.empty(n_q, H * D, device=q.device)
+    pos = torch.arange(n_q, device=q.device) + p_pre
+    keys = torch.arange(n_keys, device=q.device)
+    mask = keys[None, :] <= (pos[:, None] + mask_shift)
+    if drop_tile is not None:
+        mask &= ~((keys >= drop_tile * 128) & (keys < (drop_tile + 1) * 128))[None, :]
+    for h in range(H):
+        sl = slice(h * D, (h + 1) * D)
+        s = (q[:, sl] @ K[:, sl].T) / D ** 0.5
+        s = s.masked_fill(~mask, float("-inf"))
+        out[:, sl] = torch.softmax(s, dim=-1) @ V[:, sl]
+    return out
+
+
+def _rel_rows(out, ref, H, D):
+    """per (row, head): ||out - ref||_inf / ||ref||_inf, max over all"""
+    o = out.view(out.shape[0], H, D)
+    r = ref.view(ref.shape[0], H, D)
+    num = (o - r).abs().amax(dim=2)
+    den = r.abs().amax(dim=2).clamp_min(1e-30)
+    return (num / den).max().item()
+
+
+SHAPES = [(2, 128, 32, 1000, 72), (4, 64, 16, 0, 130), (1, 32, 8, 333, 5), (2, 16, 32, 4096, 64),
+          (1, 8, 4, 17, 3), (2, 128, 64, 20000, 72), (4, 128, 32, 5000, 300), (1, 64, 8, 3000, 1),
+          (3, 128, 16, 777, 129), (2, 64, 64, 0, 1000), (2, 128, 32, 4096, 200)]
+
+
+@pytest.mark.parametrize("H,D,S,p_pre,n_q", SHAPES)
+def test_paged_attention_relative_bar_peaked_and_poisoned(H, D, S, p_pre, n_q):
+    d, L, layer = H * D, 2, 1
+    n_keys = p_pre + n_q
+    n_pages = (n_keys + S - 1) // S
+    P = n_pages + 7
+    g = torch.Generator(device="cuda").manual_seed(H * 1000 + D + n_q)
+    pool = torch.full((L, P, 2, S, d), 0.0, device="cuda")
+    pool[:, :, 0] = POISON_K  # every slot poisoned; the live keys overwrite theirs below
+    pool[:, :, 1] = POISON_V
+    perm = torch.randperm(P, device="cuda", generator=g)
+    pages = perm[:n_pages].to(torch.int32)
+    K = torch.randn(n_keys, d, device="cuda", generator=g) * 0.5
+    V = torch.randn(n_keys, d, device="cuda", generator=g) * 0.5
+    # planted keys among the fresh rows: huge logits for the rows at or after them
+    rng = np.random.default_rng(n_q)
+    planted = sorted(set(int(p_pre + x) for x in rng.integers(0, n_q, size=min(4, n_q))))
+    for t in planted:
+        K[t] = POISON_K / 10 * torch.sign(torch.randn(d, device="cuda", generator=g))
+        V[t] = 50.0
+    for i in range(n_pages):  # live keys into their pages (padding past n_keys stays poisoned)
+        a, b = i * S, min((i + 1) * S, n_keys)
+        pool[layer, pages[i].long(), 0, : b - a] = K[a:b]
+        pool[layer, pages[i].long(), 1, : b - a] = V[a:b]
+    pool = pool.to(torch.bfloat16)
+    q = (torch.randn(n_q, d, device="cuda", generator=g) * 6.0).to(torch.bfloat16)  # scores std ~3
+    out = torch.empty(n_q, d, device="cuda", dtype=torch.float32)
+    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=S, chunk_size=S, device_pages=P))
+    rc = mtkv.lib().mtkv_op_paged_attention(out.data_ptr(), q.data_ptr(), pool.data_ptr(), pages.data_ptr(),
+                                            n_q, p_pre, n_keys, layer, mtkv.C.byref(kv._c()), P,
+                                            torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, mtkv._err()
+    torch.cuda.synchronize()
+    pl = pages.long()
+    Kb = pool[layer, pl, 0].reshape(-1, d)[:n_keys].float()
+    Vb = pool[layer, pl, 1].reshape(-1, d)[:n_keys].float()
+    qf = q.float()
+    ref = _ref_attention(qf, Kb, Vb, n_keys, p_pre, H, D)
+    rel = _rel_rows(out, ref, H, D)
+    print(f"attention H={H} D={D} S={S} p_pre={p_pre} n_q={n_q}: max rel (row,head) err {rel:.2e}")
+    assert torch.isfinite(out).all()
+    assert rel <= ATTN_REL
+    # the bar can fail: a reference with one key tile dropped / the mask shifted by one
+    if n_keys > 128:
+        bad = _ref_attention(qf, Kb, Vb, n_keys, p_pre, H, D, drop_tile=(n_keys - 1) // 128 // 2)
+        assert _rel_rows(bad, ref, H, D) > 10 * ATTN_REL
+    if n_q > 1 and planted and planted[-1] > p_pre:
+        bad = _ref_attention(qf, Kb, Vb, n_keys, p_pre, H, D, mask_shift=1)
+        assert _rel_rows(bad, ref, H, D) > 10 * ATTN_REL
+    assert _rel_rows(torch.zeros_like(out), ref, H, D) > 10 * ATTN_REL
+
+
+def _configs1_trace(users=32, history=4096, delta=64, cands=8, vocab=4096, rounds=4, seed=0):
+    rng = np.random.default_rng(seed)
+    tr = []
+    t = 0
+    for u in range(users):
+        tr.append({"ts": t, "user": u, "dn": history, "nc": cands,
+                   "tokens": rng.integers(0, vocab, history).tolist(), "cands": rng.integers(0, vocab, cands).tolist()})
+        t += 1
+    for _ in range(rounds):  # every round visits all users: with a pool of ~8 users every revisit misses HBM
+        for u in rng.permutation(users):
+            tr.append({"ts": t, "user": int(u), "dn": delta, "nc": cands,
+                       "tokens": rng.integers(0, vocab, delta).tolist(),
+                       "cands": rng.integers(0, vocab, cands).tolist()})
+            t += 1
+    return tr
+
+
+def test_value_engine_configs1_dims_evict_onload_all_modes_vs_fp64():
+    L, H, D, V = 4, 2, 128, 4096
+    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=32, chunk_size=128, device_pages=1200,
+                  offload_quota=128 * 64 * 4))
+    mc = mtkv.ModelConfig(num_layers=L, num_heads=H, head_dim=D, vocab=V, seed=1)
+    trace = _configs1_trace(vocab=V)
+    srv = RefServer(RefModel(ModelParams(num_layers=L, num_heads=H, head_dim=D, vocab=V, seed=1), device="cuda"))
+    ref = [srv.serve(r["user"], r["tokens"], r["cands"]).cpu().numpy() for r in trace]
+    bs_of = lambda i: 4 if i < 32 else 8
+    got = {}
+    for mode in ("hierarchical", "gpu_only", "recompute"):
+        eng = mtkv.Engine(kv, mode=mode, backend="value", batch_size=8, model=mc, keep_logits=True)
+        out, i = [], 0
+        while i < len(trace):
+            b = trace[i:i + bs_of(i)]
+            eng.process_batch(b)
+            out.extend(np.asarray(eng.last_logits(), dtype=np.float64))
+            i += len(b)
+        rep = eng.report()
+        rel = np.array([np.abs(g - r).max() / np.abs(r).max() for g, r in zip(out, ref)])
+        ab = np.array([np.abs(g - r).max() for g, r in zip(out, ref)])
+        print(f"{mode}: {len(out)} requests, evictions {rep['evictions']}, host-onloaded tokens "
+              f"{rep['hist_host']}, per-request rel err max {rel.max():.3e} mean {rel.mean():.3e} "
+              f"(revisits max {rel[32:].max():.3e}), abs err max {ab.max():.3e}")
+        if mode == "hierarchical":
+            assert rep["evictions"] > 0 and rep["hist_host"] > 0  # the evict -> onload path ran
+        assert rel.max() <= LOGIT_REL
+        got[mode] = out
+    for a, b in [("hierarchical", "gpu_only"), ("hierarchical", "recompute"), ("gpu_only", "recompute")]:
+        x = max(np.abs(g - h).max() / np.abs(r).max() for g, h, r in zip(got[a], got[b], ref))
+        print(f"mode invariance {a} vs {b}: max rel {x:.3e}")
+        assert x <= MODE_REL

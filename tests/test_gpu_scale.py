@@ -1,0 +1,121 @@
+"""Trace-scale parity on the B200 (tools/make_golden_scale.py fixtures, made by
+the unmodified reference):
+
+* the configs[1] request stream exactly as bench.py serves it in the driver's
+  run (2048 users x 4096-token prefill, 113 revisit batches of 64, pool 10 %),
+* the reference acceptance traces: criterion 6 (kuairand1k, DevicePages
+  5120..81920) and criterion 7 (kuairand1k and mt, batch 1/4/8, all modes),
+
+replayed through the GPU engine (tag backend) with the host planner and with
+the device planner (devctl.cu). Bars:
+  * control plane: the complete state image after EVERY batch equals the
+    reference's (chained SHA-256, checked every 64 batches), rejected batches,
+    drained final state and RunReport identical;
+  * data movement: the conservation read-back (every resident token of every
+    user on the device pool and every host chunk, byte for byte) passes at
+    several points of every run and after the drain;
+  * the reference's own acceptance criteria 6 and 7 hold on the engine's reports.
+"""
+import hashlib
+
+import pytest
+
+import paper_2604_22881_b200 as mtkv
+from oracle.oracle import StateChain
+from tests import scale_traces as st
+from tests.util import REPORT_KEYS, SCALE_CASES, scale_case
+
+pytestmark = pytest.mark.gpu
+
+N_CHECKS = 4  # conservation read-backs per run besides the final one
+
+
+def _kv(case, run):
+    kv = {**mtkv.KVConfig().__dict__, **case["kv"]}
+    if "device_pages" in run:
+        kv["device_pages"] = run["device_pages"]
+    return mtkv.KVConfig(**kv)
+
+
+def _engine(case, run, planner):
+    kv = _kv(case, run)
+    opts = dict(mode=run["mode"], backend="tag", batch_size=run["batch_size"], planner=planner)
+    if planner == "device":
+        opts.update(max_users=4096, max_user_pages=1024)
+    return mtkv.Engine(kv, mtkv.CostModel(**case["cost"]), **opts)
+
+
+def replay(eng, batches, run):
+    ch = StateChain(run["every"])
+    check_at = {len(batches) * (k + 1) // (N_CHECKS + 1) for k in range(N_CHECKS)}
+    for i, b in enumerate(batches):
+        rej = False
+        try:
+            eng.process_batch(b)
+        except mtkv.BatchRejected:
+            rej = True
+        ch.add(eng.state_blob(), rej)
+        if i in check_at and run["mode"] != "recompute":
+            eng.check_conservation()
+    samples = ch.finish()
+    n_ok = 0
+    while n_ok < len(samples) and n_ok < len(run["chain"]) and samples[n_ok] == run["chain"][n_ok]:
+        n_ok += 1
+    assert ch.n == run["n_batches"]
+    assert samples == run["chain"], f"state diverges in batches [{64 * n_ok}, {64 * (n_ok + 1)})"
+    assert ch.rejected == run["rejected"]
+    eng.drain()
+    assert hashlib.sha256(eng.state_blob()).hexdigest() == run["final_digest"]
+    if run["mode"] != "recompute":
+        eng.check_conservation()
+    rep = eng.report()
+    for k in REPORT_KEYS:
+        assert rep[k] == run["report"][k], k
+    assert eng.kernel_launches() > 0
+    return rep
+
+
+def _criteria(name, reps):
+    if name == "scale_c6":  # acceptance.cpp:283-309
+        sweep = [r for run, r in reps if run["mode"] == "hierarchical"]
+        re = [r for run, r in reps if run["mode"] == "recompute"][0]
+        for a, b in zip(sweep, sweep[1:]):
+            assert b["gpu_hit_ratio"] >= a["gpu_hit_ratio"] - 1e-12
+            assert b["total_latency_ms"] <= a["total_latency_ms"] + 1e-9
+        assert sweep[0]["total_latency_ms"] < re["total_latency_ms"]
+    elif name.startswith("scale_c7"):  # acceptance.cpp:314-345
+        prev = 0.0
+        for b in (1, 4, 8):
+            lat = {run["mode"]: r["total_latency_ms"] for run, r in reps if run["batch_size"] == b}
+            assert lat["hierarchical"] < lat["gpu_only"] < lat["recompute"]
+            speedup = lat["recompute"] / lat["hierarchical"]
+            assert speedup > prev
+            prev = speedup
+
+
+@pytest.mark.parametrize("name", SCALE_CASES)
+def test_tag_engine_replays_reference_at_scale(name):
+    case = scale_case(name)
+    trace, sizes = st.build(case["trace"])
+    assert st.trace_digest(trace) == case["trace_digest"]
+    reps = []
+    for run in case["runs"]:
+        eng = _engine(case, run, "host")
+        reps.append((run, replay(eng, st.split(trace, run["batch_size"], sizes), run)))
+        del eng
+    _criteria(name, reps)
+
+
+@pytest.mark.parametrize("name", SCALE_CASES)
+def test_device_planner_replays_reference_at_scale(name):
+    case = scale_case(name)
+    trace, sizes = st.build(case["trace"])
+    ran = 0
+    for run in case["runs"]:
+        if run["mode"] == "recompute":
+            continue  # no device tables in recompute mode
+        eng = _engine(case, run, "device")
+        replay(eng, st.split(trace, run["batch_size"], sizes), run)
+        del eng
+        ran += 1
+    assert ran > 0

@@ -24,7 +24,7 @@ def golden_cases(backend=None):
     out = []
     for p in sorted(glob.glob(os.path.join(GOLDEN, "*.json"))):
         name = os.path.basename(p)[:-5]
-        if name in ("traces", "forward", "footprint"):
+        if name in ("traces", "forward", "footprint") or name.startswith("scale_"):
             continue
         g = golden(name)
         if backend is None or g["backend"] == backend:
@@ -38,3 +38,10 @@ REPORT_KEYS = ["gpu_hit_ratio", "total_hit_ratio", "tokens_processed", "eviction
 
 def batches(trace, bs):
     return [trace[i:i + bs] for i in range(0, len(trace), bs)]
+
+
+def scale_case(name: str) -> dict:
+    return golden(name)
+
+
+SCALE_CASES = ["scale_bench_c1", "scale_c6", "scale_c7_kuairand1k", "scale_c7_mt"]
