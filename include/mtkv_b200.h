@@ -143,6 +143,24 @@ mtkv_planner* mtkv_planner_create(const mtkv_kv_config* kv, const mtkv_cost_mode
 void mtkv_planner_destroy(mtkv_planner* p);
 int mtkv_planner_process_batch(mtkv_planner* p, const mtkv_request* reqs, uint32_t n);
 int mtkv_planner_drain(mtkv_planner* p);
+/* CacheManager step surface (manager.hpp:89-147) on the same host control
+ * plane, for callers that drive the manager themselves the way
+ * Engine<B>::process_batch does (sim.hpp:332-455). Request indices refer to the
+ * last prepare; its plans / evictions are read with mtkv_last_plans /
+ * mtkv_last_evictions (is_engine = 0). Errors carry the reference's messages. */
+int mtkv_planner_prepare_metadata(mtkv_planner* p, const mtkv_request* reqs, uint32_t n,
+                                  int host_enabled);                          /* manager.cpp:74 */
+uint32_t mtkv_planner_scratch_pages(const mtkv_planner* p, uint32_t req, uint32_t* out,
+                                    uint32_t cap);                            /* RequestPlan::scratch_pages */
+/* release_scratch (manager.cpp:196): the plan's scratch page ids go back to the free list */
+int mtkv_planner_release_scratch(mtkv_planner* p, const uint32_t* pages, uint32_t n);
+/* commit_onload (manager.cpp:178): device_len = reusable_len when the plan onloaded chunks */
+int mtkv_planner_commit_onload(mtkv_planner* p, uint32_t user, uint64_t reusable_len, uint32_t onload_chunks);
+int mtkv_planner_finish_append(mtkv_planner* p, uint32_t user, uint64_t appended); /* :184 */
+int mtkv_planner_advance_persisted(mtkv_planner* p, uint32_t user, uint64_t tokens); /* :190 */
+int mtkv_planner_lock_user(mtkv_planner* p, uint32_t user);                  /* manager.cpp:165 */
+int mtkv_planner_unlock_user(mtkv_planner* p, uint32_t user);                /* manager.cpp:172 */
+uint32_t mtkv_planner_last_page_len(const mtkv_planner* p, uint32_t user);   /* manager.cpp:210 */
 
 /* ---- engine: sim.hpp:110 Engine<B> on the GPU ---- */
 typedef struct mtkv_engine mtkv_engine;

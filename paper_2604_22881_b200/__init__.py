@@ -123,6 +123,9 @@ EXPORTED_SYMBOLS = [
     "mtkv_kv_config_default", "mtkv_kv_config_validate", "mtkv_parse_config_text",
     "mtkv_cost_model_default", "mtkv_pages_needed", "mtkv_persisted_prefix", "mtkv_last_error",
     "mtkv_planner_create", "mtkv_planner_destroy", "mtkv_planner_process_batch", "mtkv_planner_drain",
+    "mtkv_planner_prepare_metadata", "mtkv_planner_scratch_pages", "mtkv_planner_release_scratch",
+    "mtkv_planner_commit_onload", "mtkv_planner_finish_append", "mtkv_planner_advance_persisted",
+    "mtkv_planner_lock_user", "mtkv_planner_unlock_user", "mtkv_planner_last_page_len",
     "mtkv_engine_create", "mtkv_engine_destroy", "mtkv_engine_process_batch", "mtkv_engine_run",
     "mtkv_engine_drain", "mtkv_engine_synchronize", "mtkv_engine_last_logits",
     "mtkv_engine_last_rankings", "mtkv_engine_batch_rankings", "mtkv_engine_batches_submitted",

@@ -158,6 +158,42 @@ int mtkv_planner_drain(mtkv_planner* p) {
   return MTKV_OK;
 }
 
+int mtkv_planner_prepare_metadata(mtkv_planner* p, const mtkv_request* reqs, uint32_t n, int host_enabled) {
+  std::string err;
+  const int rc = p->p.mgr_prepare(reqs, n, host_enabled != 0, err);
+  return rc ? fail(rc, err) : MTKV_OK;
+}
+
+uint32_t mtkv_planner_scratch_pages(const mtkv_planner* p, uint32_t req, uint32_t* out, uint32_t cap) {
+  const std::vector<uint32_t>* v = p->p.mgr_scratch(req);
+  if (!v) return 0;
+  for (uint32_t i = 0; out && i < v->size() && i < cap; ++i) out[i] = (*v)[i];
+  return uint32_t(v->size());
+}
+
+#define MTKV_STEP(call)            \
+  do {                             \
+    std::string err;               \
+    const int rc = (call);         \
+    return rc ? fail(rc, err) : MTKV_OK; \
+  } while (0)
+
+int mtkv_planner_release_scratch(mtkv_planner* p, const uint32_t* pages, uint32_t n) {
+  MTKV_STEP(p->p.mgr_release_pages(pages, n, err));
+}
+int mtkv_planner_commit_onload(mtkv_planner* p, uint32_t user, uint64_t reusable_len, uint32_t onload_chunks) {
+  MTKV_STEP(p->p.mgr_commit_onload(user, reusable_len, onload_chunks, err));
+}
+int mtkv_planner_finish_append(mtkv_planner* p, uint32_t user, uint64_t appended) {
+  MTKV_STEP(p->p.mgr_finish_append(user, appended, err));
+}
+int mtkv_planner_advance_persisted(mtkv_planner* p, uint32_t user, uint64_t tokens) {
+  MTKV_STEP(p->p.mgr_advance_persisted(user, tokens, err));
+}
+int mtkv_planner_lock_user(mtkv_planner* p, uint32_t user) { MTKV_STEP(p->p.mgr_lock(user, true, err)); }
+int mtkv_planner_unlock_user(mtkv_planner* p, uint32_t user) { MTKV_STEP(p->p.mgr_lock(user, false, err)); }
+uint32_t mtkv_planner_last_page_len(const mtkv_planner* p, uint32_t user) { return p->p.last_page_len(user); }
+
 // ----------------------------------------------------------------- engine --
 mtkv_engine* mtkv_engine_create(const mtkv_kv_config* kv, const mtkv_cost_model* cost,
                                 const mtkv_engine_options* opts) {

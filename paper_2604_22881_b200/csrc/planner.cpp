@@ -198,6 +198,152 @@ void Planner::trigger_offloads(int s, double t, BatchWork& w) {
   }
 }
 
+// prepare_metadata (manager.cpp:74): touch + LRU, hit class, page growth and
+// candidate scratch with ensure_free's evictions (manager.cpp:55), in request
+// order; a repeated user plans against its earlier occurrence's projection.
+bool Planner::prepare_metadata(const mtkv_request* reqs, uint32_t n, bool hier, std::vector<int>& slot,
+                               std::vector<uint32_t>& scratch_ids, BatchWork& w) {
+  for (uint32_t i = 0; i < n; ++i) slot[i] = slot_of(reqs[i].user, true);
+  std::vector<char> in_batch(users_.size(), 0);
+  for (uint32_t i = 0; i < n; ++i) in_batch[slot[i]] = 1;
+  // projected (total_len, device_len) per distinct user, in request order
+  std::unordered_map<int, std::pair<uint64_t, uint64_t>> proj;
+  uint64_t batch_need = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    UserRec& u = users_[slot[i]];
+    u.known = true;
+    u.last_access = ++stamp_;
+    lru_front(slot[i]);
+    auto pit = proj.try_emplace(slot[i], u.total_len, u.device_len).first;
+    const uint64_t prior = pit->second.first, devlen = pit->second.second;
+    mtkv_request_plan& p = w.reqs[i].plan;
+    p = mtkv_request_plan{};
+    p.user = reqs[i].user;
+    p.history_len = prior;
+    p.delta = reqs[i].new_token_count;
+    p.num_candidates = reqs[i].candidate_count;
+    if (p.num_candidates < 1) {
+      w.rc = MTKV_ERROR;
+      w.error = "request: need at least one candidate";
+      return false;
+    }
+    if (devlen > 0) {
+      p.device_served = std::min(devlen, prior);
+      p.reusable_len = p.device_served;
+    } else if (hier && u.persisted_len > 0) {
+      p.host_onload = u.persisted_len;
+      p.reusable_len = u.persisted_len;
+      p.onload_chunks = uint32_t(u.persisted_len / kv_.chunk_size);
+    }
+    p.fresh_history = prior - p.reusable_len;
+    const uint64_t target = prior + p.delta;
+    const uint64_t want = div_up(target, kv_.page_size);
+    const uint64_t have = u.has_pages ? u.pages.size() : 0;
+    const uint64_t grow = want > have ? want - have : 0;
+    const uint64_t scratch = div_up(p.num_candidates, kv_.page_size);
+    batch_need += grow + scratch;
+    if (batch_need > kv_.device_pages) {
+      w.rc = MTKV_BATCH_REJECTED;
+      w.error = "batch exceeds total device pages";
+      return false;
+    }
+    w.rc = free_pages_for(grow + scratch, in_batch, w);
+    if (w.rc) return false;
+    UserRec& uu = users_[slot[i]];
+    uu.has_pages = true;
+    for (uint64_t g = 0; g < grow; ++g) uu.pages.push_back(pop_page());
+    w.reqs[i].scratch_off = uint32_t(scratch_ids.size());
+    w.reqs[i].n_scratch = uint32_t(scratch);
+    for (uint64_t g = 0; g < scratch; ++g) scratch_ids.push_back(pop_page());
+    p.scratch_pages = uint32_t(scratch);
+    pit->second = {target, p.reusable_len + p.fresh_history + p.delta};
+  }
+  return true;
+}
+
+// ---- CacheManager step surface (manager.hpp:89-147): prepare_metadata and the
+// calls Engine<B>::process_batch makes after it, one at a time, for callers that
+// drive the manager themselves (the reference's manager tests do).
+int Planner::mgr_prepare(const mtkv_request* reqs, uint32_t n, bool host_enabled, std::string& err) {
+  BatchWork w;
+  w.reqs.resize(n);
+  std::vector<int> slot(n);
+  std::vector<uint32_t> ids;
+  const bool ok = prepare_metadata(reqs, n, host_enabled, slot, ids, w);
+  if (!ok && w.rc == MTKV_BATCH_REJECTED) {  // the reference keeps what happened before the throw
+    err = w.error;
+    last_ = w;
+    last_.reqs.clear();
+    return MTKV_BATCH_REJECTED;
+  }
+  if (!ok) { err = w.error; return w.rc ? w.rc : MTKV_ERROR; }
+  mgr_scratch_.assign(n, {});
+  for (uint32_t i = 0; i < n; ++i) {
+    w.reqs[i].slot = uint32_t(slot[i]);
+    mgr_scratch_[i].assign(ids.begin() + w.reqs[i].scratch_off, ids.begin() + w.reqs[i].scratch_off + w.reqs[i].n_scratch);
+  }
+  last_ = w;
+  return MTKV_OK;
+}
+
+const std::vector<uint32_t>* Planner::mgr_scratch(uint32_t i) const {
+  return i < mgr_scratch_.size() ? &mgr_scratch_[i] : nullptr;
+}
+
+int Planner::mgr_release_pages(const uint32_t* pages, uint32_t n, std::string& err) {
+  for (uint32_t i = 0; i < n; ++i) {  // alloc_.release (store.hpp:76) of each scratch page
+    if (pages[i] >= kv_.device_pages) { err = "device store: releasing free page"; return MTKV_ERROR; }
+    push_page(pages[i]);
+  }
+  return MTKV_OK;
+}
+
+int Planner::mgr_commit_onload(uint32_t user, uint64_t reusable_len, uint32_t onload_chunks, std::string& err) {
+  if (onload_chunks == 0) return MTKV_OK;  // manager.cpp:179 no pending onload: no-op
+  const int s = slot_of(user, false);
+  if (s < 0 || !users_[s].known) { err = "commit_onload: unknown user"; return MTKV_ERROR; }
+  users_[s].device_len = reusable_len;
+  return MTKV_OK;
+}
+
+int Planner::mgr_finish_append(uint32_t user, uint64_t appended, std::string& err) {
+  const int s = slot_of(user, false);
+  if (s < 0 || !users_[s].known) { err = "finish_append: unknown user"; return MTKV_ERROR; }
+  UserRec& u = users_[s];
+  u.device_len += appended;
+  u.total_len = std::max(u.total_len, u.device_len);
+  return MTKV_OK;
+}
+
+int Planner::mgr_advance_persisted(uint32_t user, uint64_t tokens, std::string& err) {
+  const int s = slot_of(user, false);
+  if (s < 0 || !users_[s].known) { err = "advance_persisted: unknown user"; return MTKV_ERROR; }
+  UserRec& u = users_[s];
+  u.persisted_len += tokens;
+  if (u.persisted_len > u.total_len) { err = "persist: beyond total length"; return MTKV_ERROR; }
+  return MTKV_OK;
+}
+
+int Planner::mgr_lock(uint32_t user, bool lock, std::string& err) {
+  const int s = slot_of(user, false);
+  if (lock) {
+    if (s < 0 || !users_[s].known) { err = "lock: unknown user"; return MTKV_ERROR; }
+    if (users_[s].locked) { err = "lock: user already locked"; return MTKV_ERROR; }
+  } else if (s < 0 || !users_[s].locked) {
+    err = "unlock: user not locked";
+    return MTKV_ERROR;
+  }
+  users_[s].locked = lock;
+  return MTKV_OK;
+}
+
+uint32_t Planner::last_page_len(uint32_t user) const {
+  const UserRec* u = find(user);
+  if (!u || u->device_len == 0) return 0;
+  const uint32_t rem = uint32_t(u->device_len % kv_.page_size);
+  return rem == 0 ? kv_.page_size : rem;
+}
+
 void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
   w = BatchWork();
   if (n == 0) return;
@@ -216,61 +362,7 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
     if (!prepare_on_device(reqs, n, slot, scratch_ids, w)) return;
     st[0] = cost_.meta_fixed;
   } else if (cached) {
-    for (uint32_t i = 0; i < n; ++i) slot[i] = slot_of(reqs[i].user, true);
-    std::vector<char> in_batch(users_.size(), 0);
-    for (uint32_t i = 0; i < n; ++i) in_batch[slot[i]] = 1;
-    // projected (total_len, device_len) per distinct user, in request order
-    std::unordered_map<int, std::pair<uint64_t, uint64_t>> proj;
-    uint64_t batch_need = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-      UserRec& u = users_[slot[i]];
-      u.known = true;
-      u.last_access = ++stamp_;
-      lru_front(slot[i]);
-      auto pit = proj.try_emplace(slot[i], u.total_len, u.device_len).first;
-      const uint64_t prior = pit->second.first, devlen = pit->second.second;
-      mtkv_request_plan& p = w.reqs[i].plan;
-      p = mtkv_request_plan{};
-      p.user = reqs[i].user;
-      p.history_len = prior;
-      p.delta = reqs[i].new_tokens ? reqs[i].new_token_count : reqs[i].new_token_count;
-      p.num_candidates = reqs[i].candidate_count;
-      if (p.num_candidates < 1) {
-        w.rc = MTKV_ERROR;
-        w.error = "request: need at least one candidate";
-        return;
-      }
-      if (devlen > 0) {
-        p.device_served = std::min(devlen, prior);
-        p.reusable_len = p.device_served;
-      } else if (hier && u.persisted_len > 0) {
-        p.host_onload = u.persisted_len;
-        p.reusable_len = u.persisted_len;
-        p.onload_chunks = uint32_t(u.persisted_len / kv_.chunk_size);
-      }
-      p.fresh_history = prior - p.reusable_len;
-      const uint64_t target = prior + p.delta;
-      const uint64_t want = div_up(target, kv_.page_size);
-      const uint64_t have = u.has_pages ? u.pages.size() : 0;
-      const uint64_t grow = want > have ? want - have : 0;
-      const uint64_t scratch = div_up(p.num_candidates, kv_.page_size);
-      batch_need += grow + scratch;
-      if (batch_need > kv_.device_pages) {
-        w.rc = MTKV_BATCH_REJECTED;
-        w.error = "batch exceeds total device pages";
-        return;
-      }
-      w.rc = free_pages_for(grow + scratch, in_batch, w);
-      if (w.rc) return;
-      UserRec& uu = users_[slot[i]];
-      uu.has_pages = true;
-      for (uint64_t g = 0; g < grow; ++g) uu.pages.push_back(pop_page());
-      w.reqs[i].scratch_off = uint32_t(scratch_ids.size());
-      w.reqs[i].n_scratch = uint32_t(scratch);
-      for (uint64_t g = 0; g < scratch; ++g) scratch_ids.push_back(pop_page());
-      p.scratch_pages = uint32_t(scratch);
-      pit->second = {target, p.reusable_len + p.fresh_history + p.delta};
-    }
+    if (!prepare_metadata(reqs, n, hier, slot, scratch_ids, w)) return;
     st[0] = cost_.meta_fixed;
   } else {
     for (uint32_t i = 0; i < n; ++i) {

@@ -89,6 +89,16 @@ class Planner {
 
   // manager surface
   int evict(uint32_t user, std::string& err);
+  // CacheManager step surface (manager.hpp:103-126); request indices refer to
+  // the last mgr_prepare
+  int mgr_prepare(const mtkv_request* reqs, uint32_t n, bool host_enabled, std::string& err);
+  const std::vector<uint32_t>* mgr_scratch(uint32_t i) const;
+  int mgr_release_pages(const uint32_t* pages, uint32_t n, std::string& err);
+  int mgr_commit_onload(uint32_t user, uint64_t reusable_len, uint32_t onload_chunks, std::string& err);
+  int mgr_finish_append(uint32_t user, uint64_t appended, std::string& err);
+  int mgr_advance_persisted(uint32_t user, uint64_t tokens, std::string& err);
+  int mgr_lock(uint32_t user, bool lock, std::string& err);
+  uint32_t last_page_len(uint32_t user) const;
   const UserRec* find(uint32_t user) const;
   std::vector<uint32_t> known_users() const;
   std::vector<uint32_t> lru_snapshot() const;
@@ -113,6 +123,8 @@ class Planner {
   void push_page(uint32_t p);
   bool evict_slot(int s, uint64_t* freed, std::string& err);
   int free_pages_for(uint64_t need, const std::vector<char>& in_batch, BatchWork& w);
+  bool prepare_metadata(const mtkv_request* reqs, uint32_t n, bool hier, std::vector<int>& slot,
+                        std::vector<uint32_t>& scratch_ids, BatchWork& w);
   bool prepare_on_device(const mtkv_request* reqs, uint32_t n, std::vector<int>& slot,
                          std::vector<uint32_t>& scratch_ids, BatchWork& w);
   void note_update(int s);  // persisted length / lock bit changed on the host
@@ -159,6 +171,7 @@ class Planner {
   uint64_t required_ = 0, dev_served_ = 0, host_served_ = 0, processed_ = 0, requests_ = 0,
            batches_ = 0, peak_pages_ = 0;
   BatchWork last_;
+  std::vector<std::vector<uint32_t>> mgr_scratch_;  // step surface: scratch ids per request
   DevCtl* ctl_ = nullptr;
   std::vector<CtlUpd> ctl_upd_;  // host-side changes queued for the next device prepare
   std::unordered_map<int, size_t> ctl_upd_at_;
