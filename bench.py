@@ -16,8 +16,8 @@ engine, then W revisit batches. Timed: K revisit batches. Synthetic data
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 N > 1: launched by torchrun, one process per GPU; users are sharded by
-user id (u -> u*N + rank), each rank owns an independent cache shard; no
-collective on the data path ("scaling": "weak").
+user-id hash (paper_2604_22881_b200.shard.shard_of), each rank owns an
+independent cache shard; no collective on the data path ("scaling": "weak").
 
 Phases: A = device throughput (`value`, pre-packed requests, CUDA events);
 B = per-batch latency (p50/p99) with per-kernel CUDA-event timing of the
@@ -160,9 +160,17 @@ def make_workload(cfg: dict, n_batches: int, rank: int, world: int, seed: int = 
     soon — the temporal locality the LRU policy exploits. The first part of the
     stream is consumed as warm-up so the timed phases see the steady state."""
     import paper_2604_22881_b200 as mtkv
+    from paper_2604_22881_b200.shard import shard_of
     rng = np.random.default_rng(seed + 7919 * rank)
     U, V = cfg["users"], cfg["vocab"]
-    uid = lambda u: u * world + rank  # user-id sharding across ranks
+    # user-id hash sharding across ranks (paper_2604_22881_b200.shard): this
+    # rank's users are the first U ids that hash to it
+    ids, u = [], 0
+    while len(ids) < U:
+        if shard_of(u, world) == rank:
+            ids.append(u)
+        u += 1
+    uid = lambda u: ids[u]
     prefill = [{"ts": 0, "user": uid(u), "dn": cfg["history"], "nc": cfg["cands"],
                 "tokens": rng.integers(0, V, cfg["history"], dtype=np.uint32),
                 "cands": rng.integers(0, V, cfg["cands"], dtype=np.uint32)} for u in range(U)]
@@ -255,9 +263,10 @@ def run_b200(args, cfg):
     extent_mb = -(-((cfg["history"] + 16 * cfg["delta"]) * tok_bytes) // 2**20)
     host_mb = int(1.1 * cfg["users"] * extent_mb) + 1024
     ppu = -(-(cfg["history"] + 16 * cfg["delta"]) // cfg["page"])
-    eng = mtkv.Engine(kv, cost, mode="hierarchical", backend="value", batch_size=B, model=model,
-                      device=local, host_reserve_mb=host_mb, host_extent_mb=extent_mb, planner=args.planner,
-                      max_users=cfg["users"] + 64, max_user_pages=2 * ppu + 64)
+    hier = args.mode == "hierarchical"
+    eng = mtkv.Engine(kv, cost, mode=args.mode, backend="value", batch_size=B, model=model,
+                      device=local, host_reserve_mb=host_mb if hier else 0, host_extent_mb=extent_mb,
+                      planner=args.planner, max_users=cfg["users"] + 64, max_user_pages=2 * ppu + 64)
     # ---- warm-up: prefill histories (untimed), then the first revisit batches ----
     pb = max(1, 65536 // cfg["history"])
     for i in range(0, len(prefill), pb):
@@ -414,8 +423,12 @@ def run_b200(args, cfg):
         "data": "synthetic (random token ids, reference-initialised random weights)",
         "config": {"workload": f"{CONFIG_TAG[args.config]} {args.config}: {cfg['L']} layers d={cfg['H'] * cfg['D']}, "
                                f"{cfg['history']}-token histories, {cfg['delta']} new + {cfg['cands']} "
-                               f"candidates/request, HBM pool {int(cfg['pool_frac'] * 100)}% of users, "
-                               f"pinned-host tier, hierarchical",
+                               f"candidates/request, " + (
+                                   "no cache (recompute every history)" if args.mode == "recompute" else
+                                   f"HBM pool {cfg['pool_frac'] * 100:g}% of users, " + (
+                                       "pinned-host tier, hierarchical" if args.mode == "hierarchical"
+                                       else "no host tier (gpu_only)")),
+                   "mode": args.mode, "pool_frac": cfg["pool_frac"],
                    "users_per_gpu": cfg["users"], "batch": B, "device_pages": kv.device_pages,
                    "page_size": cfg["page"], "chunk_size": cfg["chunk"], "parallelism": f"user-shard x{world}",
                    "warmup_batches_effective": warm,
@@ -533,12 +546,18 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--planner", default="host", choices=["host", "device"],
                     help="control plane: host C++ planner or the GPU (devctl.cu) lookup/LRU/victim kernel")
+    ap.add_argument("--mode", default="hierarchical", choices=["hierarchical", "gpu_only", "recompute"],
+                    help="configs[2] ablation: cache disabled (recompute), HBM only (gpu_only) or the hierarchical cache")
+    ap.add_argument("--pool-frac", type=float, default=0.0,
+                    help="configs[4] cache-pressure sweep: HBM pool as a fraction of the user population's KV")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = dict(CONFIGS[args.config])
     if args.users:
         cfg["users"] = args.users
+    if args.pool_frac:
+        cfg["pool_frac"] = args.pool_frac
     world, rank, _ = dist_env()
     if world > 1 or rank != 0:
         args.cpu_baseline = False

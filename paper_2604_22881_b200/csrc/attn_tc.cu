@@ -288,7 +288,10 @@ using namespace tc;
 
 template <int D>
 struct TcCfg {
-  static constexpr int NB = D / 64;                      // 64-element column blocks of Q/K/V
+  // 64-element column blocks of Q/K/V. D = 32: one block holding this head and
+  // its neighbour (a 128-B swizzled row; the head's operands start SUB bytes
+  // into it, which the MMA / tcgen05.cp descriptors address like a K step)
+  static constexpr int NB = D >= 64 ? D / 64 : 1;
   static constexpr uint32_t QBLK = BM * 128;             // 128 rows x 128 B
   static constexpr uint32_t Q_BYTES = NB * QBLK;
   static constexpr uint32_t KBLK = BN * 128;             // BN keys x 128 B
@@ -309,6 +312,7 @@ struct TcCfg {
 };
 
 template <int D, bool TR, int POLY>  // TR: per-CTA event trace; POLY: k-th columns use ex2_poly (0: none)
+// D in {32, 64, 128}
 __global__ void __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map,
                    const __grid_constant__ CUtensorMap part_map, AttnArgs a) {
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(384, 1)
       const AttnPiece P = a.pieces[pc];
       const uint64_t KA = P.start + P.n_hist;
       const uint32_t user_pages = uint32_t((KA + S - 1) / S);
-      const uint32_t col = P.head * D;
+      const uint32_t col = (P.head * D) & ~63u;  // first 64-column block of this head
       auto row_of = [&](uint64_t lp) -> int {  // pool row of a logical page's K slice
         uint32_t page;
         if (lp < user_pages) page = a.pages[P.pages_off + uint32_t(lp)];
@@ -447,8 +451,8 @@ __global__ void __launch_bounds__(384, 1)
         mbar_expect_tx(&q_full[qb], Q_BYTES);
 #pragma unroll
         for (int b = 0; b < NB; ++b)
-          tma_load_2d(sQ + qb * Q_BYTES + b * QBLK, &q_map, int(P.head * D + 64 * b), int(P.q_row0 + P.qtile * BM),
-                      &q_full[qb]);
+          tma_load_2d(sQ + qb * Q_BYTES + b * QBLK, &q_map, int(((P.head * D) & ~63u) + 64 * b),
+                      int(P.q_row0 + P.qtile * BM), &q_full[qb]);
       }
     }
   } else if (warp == 1) {
@@ -467,6 +471,7 @@ __global__ void __launch_bounds__(384, 1)
       for (uint32_t pc = pb; pc < pe; ++pc) total += a.pieces[pc].hi - a.pieces[pc].lo;
       // S cursor
       uint32_t s_pc = pb, s_left = a.pieces[pb].hi - a.pieces[pb].lo, s_k = 0, s_j = 0, stk = 0, phk = 0, s_g = 0;
+      uint32_t s_sub = 0;  // D = 32: byte offset of the piece's head inside its 64-column block
       auto issue_s = [&]() {
         const uint32_t b = s_g & 1;
         ATTN_TR(9, s_g);
@@ -474,9 +479,10 @@ __global__ void __launch_bounds__(384, 1)
           // new piece: copy its Q into TMEM, in order behind the previous
           // piece's S MMAs that still read the old Q
           const uint32_t qb = s_k & 1;
+          s_sub = D < 64 ? ((a.pieces[s_pc].head * D) & 63u) * 2 : 0;
           mbar_wait(&q_full[qb], (s_k >> 1) & 1);
           tc_after();
-          const uint64_t aq = dq0 + ((qb * Q_BYTES) >> 4);
+          const uint64_t aq = dq0 + ((qb * Q_BYTES + s_sub) >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             tmem_cp_if(leader, tmem + C::Q_COL + kk * 8, aq + ((((kk / 4) * QBLK + (kk % 4) * 32)) >> 4));
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         mbar_wait(&full_k[stk], phk);
         tc_after();
-        const uint64_t bk = dk0 + ((stk * T_BYTES) >> 4);
+        const uint64_t bk = dk0 + ((stk * T_BYTES + s_sub) >> 4);
         const uint32_t d_tmem = tmem + C::S_COL + b * BN;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
@@ -510,7 +516,8 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(p_full, gg & 1);
         mbar_wait(&full_v[stv], phv);
         tc_after();
-        const uint64_t bv = dv0 + ((stv * T_BYTES) >> 4);
+        const uint32_t v_sub = D < 64 ? ((a.pieces[v_pc].head * D) & 63u) * 2 : 0;
+        const uint64_t bv = dv0 + ((stv * T_BYTES + v_sub) >> 4);
         const uint32_t a_tmem = tmem + C::S_COL + (gg & 1) * BN;  // P(gg) over S(gg)'s buffer
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
@@ -632,14 +639,24 @@ __global__ void __launch_bounds__(384, 1)
           tc_after();
           release_v();
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            if constexpr (D >= 64) {
 #pragma unroll 1
-            for (int c = 0; c < D / 64; ++c) {
-              float o[32];
-              tmem_ld32(o_col + c * 32, o);
-              tmem_wait_ld();
+              for (int c = 0; c < D / 64; ++c) {
+                float o[32];
+                tmem_ld32(o_col + c * 32, o);
+                tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] *= alpha;
-              tmem_st32(o_col + c * 32, o);
+                for (int i = 0; i < 32; ++i) o[i] *= alpha;
+                tmem_st32(o_col + c * 32, o);
+              }
+            } else {  // D = 32: 16 O columns per warpgroup
+              float o[16];
+              tmem_ld16(o_col, o);
+              tmem_wait_ld();
+              uint32_t w[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(o[i] * alpha);
+              tmem_st16(o_col, w);
             }
           }
         }
@@ -758,8 +775,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// D = 32 reads 64-column blocks (two heads): the hidden width must be a whole
+// number of blocks so the TMA boxes stay inside a row
 bool attn_tc_supported(const PoolGeom& g) {
-  return (g.D == 64 || g.D == 128) && g.S >= 8 && g.S <= BN && (BN % g.S) == 0;
+  return (g.D == 64 || g.D == 128 || (g.D == 32 && g.d % 64 == 0)) && g.S >= 8 && g.S <= BN && (BN % g.S) == 0;
 }
 
 int num_sms() {
@@ -848,7 +867,8 @@ void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, 
   }();
   AttnArgs b = a;
   if (no_trigger) b.trigger = 0;
-  if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, part_map, b, s);
+  if (a.g.D == 32) launch_tc_d<32>(pool_map, q_map, part_map, b, s);
+  else if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, part_map, b, s);
   else launch_tc_d<128>(pool_map, q_map, part_map, b, s);
 }
 

@@ -65,7 +65,9 @@ def _rel_rows(out, ref, H, D):
 
 SHAPES = [(2, 128, 32, 1000, 72), (4, 64, 16, 0, 130), (1, 32, 8, 333, 5), (2, 16, 32, 4096, 64),
           (1, 8, 4, 17, 3), (2, 128, 64, 20000, 72), (4, 128, 32, 5000, 300), (1, 64, 8, 3000, 1),
-          (3, 128, 16, 777, 129), (2, 64, 64, 0, 1000), (2, 128, 32, 4096, 200)]
+          (3, 128, 16, 777, 129), (2, 64, 64, 0, 1000), (2, 128, 32, 4096, 200),
+          # head_dim 32 on the tcgen05 kernel (d % 64 == 0): odd heads sit 64 B into a block
+          (2, 32, 16, 500, 40), (4, 32, 32, 3000, 130), (2, 32, 8, 0, 300), (6, 32, 32, 1100, 1)]
 
 
 @pytest.mark.parametrize("H,D,S,p_pre,n_q", SHAPES)

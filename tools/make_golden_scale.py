@@ -50,8 +50,41 @@ def cases():
                    runs=[dict(mode=m, batch_size=b) for b in (1, 4, 8) for m in ("hierarchical", "gpu_only", "recompute")])
 
 
+def shard_fixture(ref):
+    """scale_shards: the kuairand1k trace (criterion 6 geometry, pool 5120 pages,
+    batch 8) routed over N = 2 and 4 user-id shards (paper_2604_22881_b200.shard):
+    the reference run on each shard's sub-trace, with the sub-batches the router
+    produces from the global batches."""
+    from paper_2604_22881_b200.shard import Router
+    spec = dict(kind="preset", preset="kuairand1k", seed=1)
+    trace, _ = st.build(spec)
+    kv = dict(SMALL_KV, device_pages=5120)
+    fx = dict(name="scale_shards", trace=spec, trace_digest=st.trace_digest(trace), kv=kv, cost={}, batch=8,
+              runs=[])
+    for n in (2, 4):
+        router = Router(n)
+        subs = [[] for _ in range(n)]
+        sizes = [[] for _ in range(n)]
+        for i in range(0, len(trace), 8):
+            parts, _ = router.split(trace[i:i + 8])
+            for s_, part in enumerate(parts):
+                if part:
+                    subs[s_].extend(part)
+                    sizes[s_].append(len(part))
+        for s_ in range(n):
+            req = dict(cmd="run", backend="tag", kv=kv, cost={}, trace=subs[s_], mode="hierarchical",
+                       batch_size=8, batch_sizes=sizes[s_])
+            r = ref.run_blobs(req, every=64)
+            fx["runs"].append(dict(shards=n, shard=s_, mode="hierarchical", batch_size=8, **r))
+            print("scale_shards", n, s_, r["n_batches"], "gpu_hit %.4f" % r["report"]["gpu_hit_ratio"], flush=True)
+    with open(os.path.join(OUT, "scale_shards.json"), "w") as f:
+        json.dump(fx, f, separators=(",", ":"))
+
+
 def main(only=None):
     ref = RefLib()
+    if not only or "scale_shards" in only:
+        shard_fixture(ref)
     for case in cases():
         if only and case["name"] not in only:
             continue
