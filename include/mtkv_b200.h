@@ -99,6 +99,9 @@ typedef struct {
   uint64_t h2d_bytes, d2h_bytes, onload_chunks, offload_chunks;
   /* raw hit accounting behind the ratios (sim.hpp:70 HitAccumulator) */
   uint64_t hist_required, hist_device, hist_host;
+  /* executor: host-hit prefix tokens brought back over the host link vs re-encoded on the SMs
+     (onload_policy adaptive; the control plane counts both as host hits) */
+  uint64_t prefix_onloaded, prefix_recomputed;
 } mtkv_run_report;
 
 typedef struct {
@@ -119,7 +122,19 @@ typedef struct {
   uint32_t host_extent_mb;   /* pinned host tier: per-user extent size (0 = 8 MB); an onload is one
                                 copy-engine transfer per extent, so extents sized to a user's
                                 persisted prefix keep the host link at its large-copy peak */
+  uint32_t onload_policy;    /* 0 (MTKV_ONLOAD_ALWAYS): every host hit is onloaded over the host link,
+                                as the reference executes it. 1 (MTKV_ONLOAD_ADAPTIVE): per batch, some
+                                host-hit prefixes are re-encoded on the SMs instead, concurrently with the
+                                onloads of the others, balancing estimated link time against recompute
+                                time. Every control-plane decision, the simulated clock and the reported
+                                hit ratios are unchanged (bit-exact); only how the prefix K/V reaches its
+                                pages differs (bf16 recompute vs the stored bf16 bytes: numerics within the
+                                engine's stated tolerance; tag backend: identical bytes). */
+  double onload_gbs;         /* adaptive policy: host-link GB/s (0 = 54) */
+  double recompute_mtok_s;   /* adaptive policy: prefix re-encode rate, M tokens/s (0 = from model dims) */
 } mtkv_engine_options;
+#define MTKV_ONLOAD_ALWAYS 0
+#define MTKV_ONLOAD_ADAPTIVE 1
 
 /* ---- configuration (core.cpp) ---- */
 void mtkv_kv_config_default(mtkv_kv_config* out);                 /* core.hpp:29 defaults */
@@ -211,6 +226,9 @@ int mtkv_engine_last_chunk_copy_ms(mtkv_engine* e, double* scatter_ms, uint32_t*
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e);
 /* toggles per-launch CUDA-event timing of the attention kernels */
 void mtkv_engine_set_profile(mtkv_engine* e, uint32_t on);
+/* switches the executor's host-hit policy (mtkv_engine_options::onload_policy)
+ * from the next batch on; the control plane is unaffected */
+int mtkv_engine_set_onload_policy(mtkv_engine* e, uint32_t policy, double onload_gbs, double recompute_mtok_s);
 
 /* ---- both objects: manager state (sim.hpp:149 manager()) ----
  * `obj` is an mtkv_planner* or mtkv_engine* as named by `is_engine`. */

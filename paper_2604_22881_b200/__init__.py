@@ -99,7 +99,8 @@ class _Report(C.Structure):
                 ("quota_in_flight", C.c_uint64), ("clock", C.c_double), ("h2d_bytes", C.c_uint64),
                 ("d2h_bytes", C.c_uint64), ("onload_chunks", C.c_uint64),
                 ("offload_chunks", C.c_uint64), ("hist_required", C.c_uint64),
-                ("hist_device", C.c_uint64), ("hist_host", C.c_uint64)]
+                ("hist_device", C.c_uint64), ("hist_host", C.c_uint64),
+                ("prefix_onloaded", C.c_uint64), ("prefix_recomputed", C.c_uint64)]
 
 
 class _EngineOpts(C.Structure):
@@ -107,7 +108,8 @@ class _EngineOpts(C.Structure):
                 ("seed", C.c_uint64), ("model", _ModelCfg), ("device", C.c_int),
                 ("max_batch_tokens", C.c_uint32), ("max_user_pages", C.c_uint32),
                 ("keep_logits", C.c_uint32), ("profile", C.c_uint32), ("host_reserve_mb", C.c_uint64),
-                ("device_planner", C.c_uint32), ("max_users", C.c_uint32), ("host_extent_mb", C.c_uint32)]
+                ("device_planner", C.c_uint32), ("max_users", C.c_uint32), ("host_extent_mb", C.c_uint32),
+                ("onload_policy", C.c_uint32), ("onload_gbs", C.c_double), ("recompute_mtok_s", C.c_double)]
 
 
 class _GenCfg(C.Structure):
@@ -134,7 +136,7 @@ EXPORTED_SYMBOLS = [
     "mtkv_engine_last_batch_ms", "mtkv_engine_last_attention_ms", "mtkv_engine_last_chunk_copy_ms",
     "mtkv_engine_last_proj_ms",
     "mtkv_engine_kernel_launches",
-    "mtkv_engine_set_profile",
+    "mtkv_engine_set_profile", "mtkv_engine_set_onload_policy",
     "mtkv_report", "mtkv_last_plans", "mtkv_last_evictions", "mtkv_known_users", "mtkv_user_state",
     "mtkv_user_pages", "mtkv_lru_snapshot", "mtkv_evict_user", "mtkv_is_locked",
     "mtkv_get_total_cache_length", "mtkv_dump_page_map", "mtkv_state_blob", "mtkv_gen_config_default", "mtkv_gen_config_preset",
@@ -188,6 +190,7 @@ def lib():
         "mtkv_engine_last_chunk_copy_ms": (C.c_int, [vp, C.POINTER(C.c_double), u32p, C.POINTER(C.c_double), u32p]),
         "mtkv_engine_kernel_launches": (u64, [vp]),
         "mtkv_engine_set_profile": (None, [vp, u32]),
+        "mtkv_engine_set_onload_policy": (C.c_int, [vp, u32, C.c_double, C.c_double]),
         "mtkv_report": (C.c_int, [vp, C.c_int, C.POINTER(_Report)]),
         "mtkv_last_plans": (u32, [vp, C.c_int, C.POINTER(_Plan), u32]),
         "mtkv_last_evictions": (u32, [vp, C.c_int, C.POINTER(_Eviction), u32]),
@@ -511,7 +514,8 @@ class Engine(_ManagerView):
                  backend: str = "tag", batch_size: int = 1, model: ModelConfig | None = None,
                  device: int = 0, keep_logits: bool = False, profile: bool = False, seed: int = 1,
                  host_reserve_mb: int = 0, planner: str = "host", max_users: int = 0,
-                 max_user_pages: int = 0, host_extent_mb: int = 0):
+                 max_user_pages: int = 0, host_extent_mb: int = 0, onload_policy: str = "always",
+                 onload_gbs: float = 0.0, recompute_mtok_s: float = 0.0):
         self.kv, self.mode, self.backend, self.batch_size = kv, mode, backend, batch_size
         self.model = model
         if backend == "value" and model is None:
@@ -527,6 +531,10 @@ class Engine(_ManagerView):
         o.device_planner = int(planner == "device")
         o.max_users, o.max_user_pages = int(max_users), int(max_user_pages)
         o.host_extent_mb = int(host_extent_mb)
+        if onload_policy not in ("always", "adaptive"):
+            raise Error("onload_policy must be 'always' or 'adaptive'")
+        o.onload_policy = int(onload_policy == "adaptive")
+        o.onload_gbs, o.recompute_mtok_s = float(onload_gbs), float(recompute_mtok_s)
         self._h = lib().mtkv_engine_create(C.byref(kv._c()), C.byref((cost or CostModel())._c()),
                                            C.byref(o))
         if not self._h:
@@ -644,6 +652,13 @@ class Engine(_ManagerView):
 
     def set_profile(self, on: bool) -> None:
         lib().mtkv_engine_set_profile(self._h, int(on))
+
+    def set_onload_policy(self, policy: str, onload_gbs: float = 0.0, recompute_mtok_s: float = 0.0) -> None:
+        """'always' (every host hit onloaded, as the reference) or 'adaptive'
+        (some host-hit prefixes re-encoded on the SMs); from the next batch on."""
+        if policy not in ("always", "adaptive"):
+            raise Error("onload_policy must be 'always' or 'adaptive'")
+        _check(lib().mtkv_engine_set_onload_policy(self._h, int(policy == "adaptive"), onload_gbs, recompute_mtok_s))
 
     def kernel_launches(self) -> int:
         return int(lib().mtkv_engine_kernel_launches(self._h))

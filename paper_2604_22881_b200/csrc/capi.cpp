@@ -306,6 +306,11 @@ int mtkv_engine_last_chunk_copy_ms(mtkv_engine* e, double* scatter_ms, uint32_t*
 }
 uint64_t mtkv_engine_kernel_launches(const mtkv_engine* e) { return e->e.launches; }
 void mtkv_engine_set_profile(mtkv_engine* e, uint32_t on) { e->e.set_profile(on); }
+int mtkv_engine_set_onload_policy(mtkv_engine* e, uint32_t policy, double onload_gbs, double recompute_mtok_s) {
+  std::string err;
+  const int rc = e->e.set_onload_policy(policy, onload_gbs, recompute_mtok_s, err);
+  return rc ? fail(rc, err) : MTKV_OK;
+}
 
 // ------------------------------------------------------------ manager view --
 int mtkv_report(const void* obj, int is_engine, mtkv_run_report* out) {

@@ -241,6 +241,7 @@ int Engine::init(std::string& err) {
     }
   }
   if (value_) init_weights();
+  if (set_onload_policy(opt_.onload_policy, opt_.onload_gbs, opt_.recompute_mtok_s, err)) return MTKV_ERROR;
   if (opt_.device_planner) {
     if (recompute_) {
       err = "engine: the device planner needs a cached mode (gpu_only or hierarchical)";
@@ -373,6 +374,25 @@ int Engine::validate_payload(const mtkv_request* reqs, uint32_t n, std::string& 
     for (uint32_t j = 0; j < r.candidate_count; ++j)
       if (r.candidates[j] >= V) { err = "forward: token id out of vocabulary"; return MTKV_ERROR; }
   }
+  return MTKV_OK;
+}
+
+// Executor policy for host hits (mtkv_engine_options::onload_policy); may change
+// between batches (the control plane does not depend on it).
+int Engine::set_onload_policy(uint32_t policy, double gbs, double mtok_s, std::string& err) {
+  if (policy > MTKV_ONLOAD_ADAPTIVE) {
+    err = "engine: unknown onload_policy";
+    return MTKV_ERROR;
+  }
+  opt_.onload_policy = policy;
+  opt_.onload_gbs = gbs;
+  opt_.recompute_mtok_s = mtok_s;
+  // default re-encode rate: the layer stack's FLOPs per token (dense 12 d^2 plus
+  // attention over ~2K keys) at ~200 TFLOP/s effective (measured 38 M tok/s for
+  // 4K-token histories at L=4, d=256)
+  const double d = g_.d, flops = double(g_.L) * (12.0 * d * d + 2.0 * 2.0 * 2048.0 * d);
+  const double tps = mtok_s > 0 ? mtok_s * 1e6 : 2e14 / flops;
+  planner.set_onload_policy(int(policy), (gbs > 0 ? gbs : 54.0) * 1e9, tps);
   return MTKV_OK;
 }
 

@@ -71,6 +71,7 @@ class Engine {
   double last_proj_ms(uint32_t* launches, uint64_t* rows);
   void report(mtkv_run_report& r) const;
   void set_profile(uint32_t on) { opt_.profile = on; }
+  int set_onload_policy(uint32_t policy, double gbs, double mtok_s, std::string& err);
   uint32_t batch_size() const { return opt_.batch_size ? opt_.batch_size : 1; }
 
   Planner planner;

@@ -344,6 +344,28 @@ uint32_t Planner::last_page_len(uint32_t user) const {
   return rem == 0 ? kv_.page_size : rem;
 }
 
+// Adaptive onload policy: walk the batch's host-hit requests in order and send
+// each to whichever resource would finish it earlier — the host link (its
+// persisted chunks at link_Bps_) or the SMs (re-encoding its prefix at
+// recompute_tps_, on top of the batch's own fresh rows). The batch then costs
+// roughly max(link, SMs) instead of link + nothing.
+void Planner::choose_recompute(BatchWork& w) {
+  double t_link = 0, t_sm = 0;
+  for (const ReqWork& r : w.reqs)
+    t_sm += double(r.plan.fresh_history + r.plan.delta + r.plan.num_candidates) / recompute_tps_;
+  for (ReqWork& r : w.reqs) {
+    if (!r.plan.onload_chunks) continue;
+    const double c_link = double(r.plan.onload_chunks) * double(chunk_bytes_u64_) / link_Bps_;
+    const double c_sm = double(r.plan.reusable_len) / recompute_tps_;
+    if (t_link + c_link <= t_sm + c_sm) {
+      t_link += c_link;
+    } else {
+      r.recompute_prefix = true;
+      t_sm += c_sm;
+    }
+  }
+}
+
 void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
   w = BatchWork();
   if (n == 0) return;
@@ -412,9 +434,12 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
                    scratch_ids.begin() + r.scratch_off + r.n_scratch);
     r.scratch_off = so;
   }
+  if (hier && policy_ == MTKV_ONLOAD_ADAPTIVE) choose_recompute(w);
   for (uint32_t i = 0; i < n; ++i) {
     const ReqWork& r = w.reqs[i];
     const UserRec& u = users_[slot[i]];
+    if (r.plan.onload_chunks) (r.recompute_prefix ? prefix_recomputed_ : prefix_onloaded_) += r.plan.reusable_len;
+    if (r.recompute_prefix) continue;  // its K/V is re-encoded, nothing crosses the host link
     for (uint32_t c = 0; c < r.plan.onload_chunks; ++c) {
       ChunkMove m;
       m.chunk_id = u.host_chunks[c];
@@ -467,15 +492,17 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
     const auto& p = r.plan;
     r.tok_off = uint32_t(w.tokens.size());
     if (cached) {
-      r.start = u.device_len;
-      r.n_hist = uint32_t(p.fresh_history + p.delta);
+      // a re-encoded host-hit prefix (adaptive policy) is appended from position 0
+      const uint64_t from = r.recompute_prefix ? 0 : p.reusable_len;
+      r.start = r.recompute_prefix ? 0 : u.device_len;
+      r.n_hist = uint32_t(p.fresh_history + p.delta + (p.reusable_len - from));
       if (keep_tokens_) {
         if (u.tokens.size() != p.history_len) {
           w.rc = MTKV_ERROR;
           w.error = "value mode: trace must carry explicit token ids";
           return;
         }
-        w.tokens.insert(w.tokens.end(), u.tokens.begin() + p.reusable_len, u.tokens.end());
+        w.tokens.insert(w.tokens.end(), u.tokens.begin() + from, u.tokens.end());
       }
       u.device_len += p.fresh_history + p.delta;  // finish_append (manager.cpp:184)
       u.total_len = std::max(u.total_len, u.device_len);
@@ -660,6 +687,8 @@ void Planner::report(mtkv_run_report& r) const {
   r.hist_required = required_;
   r.hist_device = dev_served_;
   r.hist_host = host_served_;
+  r.prefix_onloaded = prefix_onloaded_;
+  r.prefix_recomputed = prefix_recomputed_;
 }
 
 }  // namespace mtkv_b200

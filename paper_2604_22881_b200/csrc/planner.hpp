@@ -55,6 +55,7 @@ struct ReqWork {
   uint32_t pages_off = 0, n_pages = 0;      // into BatchWork::pages (user page snapshot)
   uint32_t scratch_off = 0, n_scratch = 0;  // into BatchWork::pages
   uint32_t tok_off = 0;        // into BatchWork::tokens: fresh history ids ++ candidate ids
+  bool recompute_prefix = false;  // adaptive onload policy: host-hit prefix re-encoded (start = 0)
 };
 
 struct ChunkMove {
@@ -113,6 +114,14 @@ class Planner {
   // Device control plane (devctl.hpp): prepare_metadata's decisions come from the
   // GPU; this planner mirrors them and sends its own state changes back.
   void set_device_ctl(DevCtl* c) { ctl_ = c; }
+  // Executor policy for host hits (mtkv_engine_options::onload_policy): which
+  // prefixes come back over the host link and which are re-encoded on the SMs.
+  // Decisions of the control plane are unaffected.
+  void set_onload_policy(int policy, double link_bytes_per_s, double recompute_tok_per_s) {
+    policy_ = policy;
+    link_Bps_ = link_bytes_per_s;
+    recompute_tps_ = recompute_tok_per_s;
+  }
   bool device_ctl() const { return ctl_ != nullptr; }
 
  private:
@@ -173,6 +182,10 @@ class Planner {
   BatchWork last_;
   std::vector<std::vector<uint32_t>> mgr_scratch_;  // step surface: scratch ids per request
   DevCtl* ctl_ = nullptr;
+  int policy_ = MTKV_ONLOAD_ALWAYS;
+  double link_Bps_ = 54e9, recompute_tps_ = 38e6;
+  uint64_t prefix_onloaded_ = 0, prefix_recomputed_ = 0;
+  void choose_recompute(BatchWork& w);
   std::vector<CtlUpd> ctl_upd_;  // host-side changes queued for the next device prepare
   std::unordered_map<int, size_t> ctl_upd_at_;
 };

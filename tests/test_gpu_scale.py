@@ -37,9 +37,10 @@ def _kv(case, run):
     return mtkv.KVConfig(**kv)
 
 
-def _engine(case, run, planner):
+def _engine(case, run, planner, policy="always"):
     kv = _kv(case, run)
-    opts = dict(mode=run["mode"], backend="tag", batch_size=run["batch_size"], planner=planner)
+    opts = dict(mode=run["mode"], backend="tag", batch_size=run["batch_size"], planner=planner,
+                onload_policy=policy)
     if planner == "device":
         opts.update(max_users=4096, max_user_pages=1024)
     return mtkv.Engine(kv, mtkv.CostModel(**case["cost"]), **opts)
@@ -119,3 +120,23 @@ def test_device_planner_replays_reference_at_scale(name):
         del eng
         ran += 1
     assert ran > 0
+
+
+@pytest.mark.parametrize("name", ["scale_bench_c1", "scale_c6"])
+def test_adaptive_onload_policy_keeps_decisions_and_bytes(name):
+    """onload_policy=adaptive re-encodes some host-hit prefixes on the SMs instead
+    of onloading them: every control-plane decision and the report stay the
+    reference's (same chained digests), and the tag backend's conservation
+    read-back proves the re-encoded prefixes put exactly the bytes an onload would."""
+    case = scale_case(name)
+    trace, sizes = st.build(case["trace"])
+    for run in case["runs"]:
+        if run["mode"] != "hierarchical":
+            continue
+        eng = _engine(case, run, "host", policy="adaptive")
+        replay(eng, st.split(trace, run["batch_size"], sizes), run)
+        rep = eng.report()
+        print(f"{name} pool {_kv(case, run).device_pages}: prefix tokens onloaded {rep['prefix_onloaded']}, "
+              f"re-encoded {rep['prefix_recomputed']}")
+        assert rep["prefix_recomputed"] > 0 and rep["prefix_onloaded"] > 0
+        del eng
