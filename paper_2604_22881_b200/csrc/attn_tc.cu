@@ -235,6 +235,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v)) : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -292,43 +300,47 @@ struct TcCfg {
   // its neighbour (a 128-B swizzled row; the head's operands start SUB bytes
   // into it, which the MMA / tcgen05.cp descriptors address like a K step)
   static constexpr int NB = D >= 64 ? D / 64 : 1;
-  static constexpr uint32_t QBLK = BM * 128;             // 128 rows x 128 B
-  static constexpr uint32_t Q_BYTES = NB * QBLK;
   static constexpr uint32_t KBLK = BN * 128;             // BN keys x 128 B
-  static constexpr uint32_t T_BYTES = NB * KBLK;         // one K (or V) tile
+  static constexpr uint32_t T_BYTES = NB * KBLK;         // one K (or V, or Q: BM == BN) tile
+  static constexpr uint32_t QBLK = KBLK;
+  static_assert(BM == BN, "a piece's Q travels through a V ring stage");
 #ifndef MTKV_ATTN_NK
-#define MTKV_ATTN_NK 3
+#define MTKV_ATTN_NK 4
 #endif
-  static constexpr int NK = D == 128 ? MTKV_ATTN_NK : 4;      // K ring stages (128-key tiles)
-  static constexpr int NV = D == 128 ? 5 - MTKV_ATTN_NK : 4;  // V ring stages (V is held until PV)
+  // All shared memory is K/V ring: the more tiles in flight per SM, the more of
+  // the loaded DRAM latency (~3 us at full bandwidth, measured) is covered.
+  static constexpr int NK = D == 128 ? MTKV_ATTN_NK : 6;      // K ring stages (128-key tiles)
+  static constexpr int NV = D == 128 ? 7 - MTKV_ATTN_NK : 6;  // V ring stages (V is held until PV; also carries Q)
   // TMEM: two S buffers (fp32, BN cols; P(t) is written as bf16x2 over the first
-  // BN/2 columns of S(t)'s buffer), O (D cols), Q (D/2 cols)
-  static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, Q_COL = 2 * BN + D;
-  static constexpr uint32_t TMEM_COLS = Q_COL + D / 2 <= 256 ? 256 : 512;
-  static_assert(Q_COL + D / 2 <= 512, "TMEM budget");
-  static constexpr size_t SMEM = 2 * Q_BYTES + size_t(NK + NV) * T_BYTES + 2 * 2 * BM * 4 + 256;
+  // BN/2 columns of S(t)'s buffer), O (D cols), Q (D/2 cols), L (16 cols: the
+  // row sums of P, accumulated by the tensor core as P x ones)
+  static constexpr uint32_t S_COL = 0, O_COL = 2 * BN, Q_COL = 2 * BN + D, L_COL = Q_COL + D / 2;
+  static constexpr uint32_t TMEM_COLS = L_COL + 16 <= 256 ? 256 : 512;
+  static_assert(L_COL + 16 <= 512, "TMEM budget");
+  static constexpr size_t SMEM = size_t(NK + NV) * T_BYTES + 2 * 2 * BM * 4 + 128 + 256;
   static_assert(SMEM <= 232448, "shared memory budget");
-  static_assert(8 * 32 * (D / 4) * 4 <= Q_BYTES, "epilogue staging fits one Q buffer");
 };
 
 template <int D, bool TR, int POLY>  // TR: per-CTA event trace; POLY: k-th columns use ex2_poly (0: none)
 // D in {32, 64, 128}
 __global__ void __launch_bounds__(384, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap pool_map, const __grid_constant__ CUtensorMap q_map,
-                   const __grid_constant__ CUtensorMap part_map, AttnArgs a) {
+                   AttnArgs a) {
   using C = TcCfg<D>;
   constexpr int NB = C::NB, NK = C::NK, NV = C::NV;
-  constexpr uint32_t QBLK = C::QBLK, KBLK = C::KBLK, T_BYTES = C::T_BYTES, Q_BYTES = C::Q_BYTES;
+  constexpr uint32_t QBLK = C::QBLK, KBLK = C::KBLK, T_BYTES = C::T_BYTES;
   constexpr int HC = BN / 2;        // key columns per softmax warpgroup
   constexpr float kRescale = 8.f;   // lazy rescale threshold (log2 units): p <= 2^8 between rescales
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];  // 128-B swizzled tiles need 1024-B alignment
   uint8_t* smem = smem_raw;
-  uint8_t* sQ = smem;                          // [2] Q buffers (TMA target -> TMEM; then epilogue staging)
-  uint8_t* sK = sQ + 2 * Q_BYTES;              // [NK] K tiles
-  uint8_t* sV = sK + NK * T_BYTES;             // [NV] V tiles
+  uint8_t* sK = smem;                          // [NK] K tiles
+  uint8_t* sV = sK + NK * T_BYTES;             // [NV] V tiles, and each piece's Q ahead of its V tiles
   float* sMax = reinterpret_cast<float*>(sV + NV * T_BYTES);  // [2 tiles][2 warpgroups][BM] row-max exchange
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sMax + 2 * 2 * BM);
+  // 64 bf16 ones: one no-swizzle core matrix (8 rows x 16 B) that the P x ones
+  // MMA reads as every core matrix of its [128 keys x 16] B operand (strides 0)
+  uint32_t* sOnes = reinterpret_cast<uint32_t*>(sMax + 2 * 2 * BM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + 32);
   uint64_t* full_k = bars;
   uint64_t* empty_k = full_k + NK;
   uint64_t* full_v = empty_k + NK;
@@ -336,10 +348,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_full = empty_v + NV;  // [2] S buffer computed
   uint64_t* p_full = s_full + 2;    // P(t) in TMEM + O rescaled (8 softmax warps)
   uint64_t* o_done = p_full + 1;    // PV(t) completed
-  uint64_t* q_full = o_done + 1;    // [2] Q buffer landed
-  uint64_t* q_empty = q_full + 2;   // [2] Q buffer copied into TMEM
-  uint64_t* epi_done = q_empty + 2; // [2] the piece's epilogue (staged in that Q buffer) done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const PoolGeom& g = a.g;
@@ -349,21 +358,18 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t pb = a.cta_off[blockIdx.x], pe = a.cta_off[blockIdx.x + 1];
 
   if (threadIdx.x == 0) {
-    // a K stage is released by the 8 softmax warps once they hold S (so the S
-    // MMA, hence its K read, completed); a V stage once they saw that tile's PV
-    // complete — keeps commits off the MMA issuer
-    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 8); }
-    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 8); }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&q_full[b], 1);
-      mbar_init(&q_empty[b], 1);
-      mbar_init(&epi_done[b], 8);
-    }
+    // every ring stage is released by the MMA issuer's tcgen05.commit: a K stage
+    // once its S = Q K^T completed, a V stage once its PV completed, a Q stage
+    // (V ring) once tcgen05.cp moved it into TMEM
+    for (int s = 0; s < NK; ++s) { mbar_init(&full_k[s], 1); mbar_init(&empty_k[s], 1); }
+    for (int s = 0; s < NV; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], 1); }
+    for (int b = 0; b < 2; ++b) mbar_init(&s_full[b], 1);
     mbar_init(p_full, 8);
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (threadIdx.x < 32) sOnes[threadIdx.x] = 0x3F803F80u;  // bf16x2 (1, 1)
+  fence_async_smem();  // visible to the tensor core (async proxy)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tmem_slot)),
                  "n"(C::TMEM_COLS));
@@ -385,6 +391,10 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0 || warp == 3) {
     // ---------------- K / V producers (whole warp: lane i resolves page i) ----------------
+    // The V ring also carries each piece's Q tile, loaded right ahead of the
+    // piece's first V tile (Q is written by the projection GEMM: the V producer
+    // waits for it up front; V is consumed a softmax pass after K anyway, so
+    // only the K producer streams cached-prefix tiles before the GEMM retires).
     const bool isv = warp == 3;
     uint64_t* full = isv ? full_v : full_k;
     uint64_t* empty = isv ? empty_v : empty_k;
@@ -393,6 +403,22 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t ppt = BN / S;  // pages per tile
     uint32_t gt = 0, st = 0, ph = 0;
     bool dep_done = false;        // griddepcontrol.wait executed
+    if (isv) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      dep_done = true;
+    }
+    auto acquire = [&]() -> uint8_t* {  // lane 0: wait for the next stage and arm it for one tile
+      if (lane == 0) {
+        if (gt >= NS) mbar_wait(&empty[st], ph ^ 1);
+        mbar_expect_tx(&full[st], T_BYTES);
+      }
+      __syncwarp();
+      return ring + st * T_BYTES;
+    };
+    auto advance = [&]() {
+      ++gt;
+      if (++st == NS) { st = 0; ph ^= 1; }
+    };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const uint64_t KA = P.start + P.n_hist;
@@ -406,9 +432,18 @@ __global__ void __launch_bounds__(384, 1)
         else return -int(S) * 4;  // out of bounds -> TMA zero fill
         return int(((uint64_t(a.layer) * g.num_pages + page) * 2) * S);
       };
+      if (isv) {  // the piece's Q (one TMA box per 64-column block)
+        uint8_t* dst = acquire();
+        if (lane == 0) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            tma_load_2d(dst + b * QBLK, &q_map, int(col + 64 * b), int(P.q_row0 + P.qtile * BM), &full[st]);
+        }
+        advance();
+      }
       uint32_t cache_t0 = P.lo;
       int rows_cache = row_of(uint64_t(P.lo) * ppt + lane);  // 32 consecutive pages per refresh
-      for (uint32_t t = P.lo; t < P.hi; ++t, ++gt) {
+      for (uint32_t t = P.lo; t < P.hi; ++t) {
         if ((t - cache_t0) * ppt >= 32) {
           cache_t0 = t;
           rows_cache = row_of(uint64_t(t) * ppt + lane);
@@ -417,13 +452,8 @@ __global__ void __launch_bounds__(384, 1)
           asm volatile("griddepcontrol.wait;" ::: "memory");
           dep_done = true;
         }
-        if (lane == 0) {
-          if (gt >= NS) mbar_wait(&empty[st], ph ^ 1);
-          if (!isv) ATTN_TR(0, gt);
-          mbar_expect_tx(&full[st], T_BYTES);
-        }
-        __syncwarp();
-        uint8_t* dst = ring + st * T_BYTES;
+        if (!isv && lane == 0) ATTN_TR(0, gt);
+        uint8_t* dst = acquire();
         for (uint32_t i = 0; i < ppt; ++i) {
           int row = __shfl_sync(0xffffffffu, rows_cache, (t - cache_t0) * ppt + i);
           if (isv && row >= 0) row += int(S);
@@ -433,26 +463,7 @@ __global__ void __launch_bounds__(384, 1)
               tma_load_2d(dst + b * KBLK + i * S * 128, &pool_map, int(col + 64 * b), row, &full[st]);
           }
         }
-        if (++st == NS) { st = 0; ph ^= 1; }
-      }
-    }
-  } else if (warp == 2) {
-    // ---------------- Q loader: one TMA box per 64-column block, double-buffered ----------------
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // Q is written by the projection GEMM
-    if (lane == 0) {
-      uint32_t k = 0;
-      for (uint32_t pc = pb; pc < pe; ++pc, ++k) {
-        const AttnPiece P = a.pieces[pc];
-        const uint32_t qb = k & 1;
-        if (k >= 2) {
-          mbar_wait(&q_empty[qb], ((k >> 1) - 1) & 1);
-          mbar_wait(&epi_done[qb], ((k >> 1) - 1) & 1);  // piece k-2's epilogue staged in this buffer
-        }
-        mbar_expect_tx(&q_full[qb], Q_BYTES);
-#pragma unroll
-        for (int b = 0; b < NB; ++b)
-          tma_load_2d(sQ + qb * Q_BYTES + b * QBLK, &q_map, int(((P.head * D) & ~63u) + 64 * b),
-                      int(P.q_row0 + P.qtile * BM), &q_full[qb]);
+        advance();
       }
     }
   } else if (warp == 1) {
@@ -465,28 +476,41 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
       constexpr uint32_t idesc_o =
           (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(D >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-      const uint64_t dq0 = sdesc(s32(sQ), 16, 1024), dk0 = sdesc(s32(sK), 16, 1024), dv0 = sdesc(s32(sV), KBLK, 1024);
+      // row sums: L[128 x 16] += P[128 x 128 keys] x ones[128 x 16] (B K-major, no swizzle, all strides 0)
+      constexpr uint32_t idesc_l = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(16 >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+      const uint64_t d_ones = uint64_t((s32(sOnes) >> 4) & 0x3FFF) | (uint64_t(1) << 46);
+      const uint64_t dk0 = sdesc(s32(sK), 16, 1024), dq0 = sdesc(s32(sV), 16, 1024), dv0 = sdesc(s32(sV), KBLK, 1024);
       const bool leader = elect_one();
       uint32_t total = 0;
       for (uint32_t pc = pb; pc < pe; ++pc) total += a.pieces[pc].hi - a.pieces[pc].lo;
       // S cursor
-      uint32_t s_pc = pb, s_left = a.pieces[pb].hi - a.pieces[pb].lo, s_k = 0, s_j = 0, stk = 0, phk = 0, s_g = 0;
+      uint32_t s_pc = pb, s_left = a.pieces[pb].hi - a.pieces[pb].lo, s_j = 0, stk = 0, phk = 0, s_g = 0;
       uint32_t s_sub = 0;  // D = 32: byte offset of the piece's head inside its 64-column block
+      // V-ring positions: the producer fills the ring as Q(p), V tiles of p,
+      // Q(p+1), ... S runs two tiles ahead of PV, so Q(p+1) is taken (by the
+      // piece's first S) before the last V tiles of p: each side keeps its own
+      // position (stage = pos % NV, phase = pos / NV), stages are released out
+      // of order by their own commits
+      uint32_t pv_pc = pb, pv_left = a.pieces[pb].hi - a.pieces[pb].lo;  // PV-side piece cursor
+      uint32_t pv_next = 1;  // V-ring position of the next V tile (Q(pb) sits at 0)
+      uint32_t q_next = 0;   // V-ring position of the next piece's Q
       auto issue_s = [&]() {
         const uint32_t b = s_g & 1;
         ATTN_TR(9, s_g);
         if (s_j == 0) {
-          // new piece: copy its Q into TMEM, in order behind the previous
-          // piece's S MMAs that still read the old Q
-          const uint32_t qb = s_k & 1;
+          // new piece: copy its Q (V ring) into TMEM, in order behind the
+          // previous piece's S MMAs that still read the old Q
+          const uint32_t qs = q_next % NV, qph = (q_next / NV) & 1;
           s_sub = D < 64 ? ((a.pieces[s_pc].head * D) & 63u) * 2 : 0;
-          mbar_wait(&q_full[qb], (s_k >> 1) & 1);
+          mbar_wait(&full_v[qs], qph);
           tc_after();
-          const uint64_t aq = dq0 + ((qb * Q_BYTES + s_sub) >> 4);
+          const uint64_t aq = dq0 + ((qs * T_BYTES + s_sub) >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             tmem_cp_if(leader, tmem + C::Q_COL + kk * 8, aq + ((((kk / 4) * QBLK + (kk % 4) * 32)) >> 4));
-          mma_commit_if(leader, &q_empty[qb]);  // smem Q buffer reusable once copied
+          mma_commit_if(leader, &empty_v[qs]);  // stage reusable once copied
+          // the following piece's Q sits after this piece's Q and V tiles
+          q_next += 1 + (a.pieces[s_pc].hi - a.pieces[s_pc].lo);
         }
         mbar_wait(&full_k[stk], phk);
         tc_after();
@@ -497,40 +521,46 @@ __global__ void __launch_bounds__(384, 1)
           mma_ts_if(leader, d_tmem, tmem + C::Q_COL + kk * 8, bk + (((kk / 4) * KBLK + (kk % 4) * 32) >> 4), idesc_s,
                     kk > 0);
         mma_commit_if(leader, &s_full[b]);
+        mma_commit_if(leader, &empty_k[stk]);  // K stage read once S completed
         if (leader) ATTN_TR(1, s_g);
         if (++stk == NK) { stk = 0; phk ^= 1; }
         ++s_g;
         ++s_j;
         if (--s_left == 0) {
           ++s_pc;
-          ++s_k;
           s_j = 0;
           if (s_pc < pe) { const AttnPiece Pn = a.pieces[s_pc]; s_left = Pn.hi - Pn.lo; }
         }
       };
       issue_s();
       if (s_g < total) issue_s();
-      uint32_t v_pc = pb, v_left = a.pieces[pb].hi - a.pieces[pb].lo, v_j = 0, stv = 0, phv = 0;
+      uint32_t v_j = 0;
       for (uint32_t gg = 0; gg < total; ++gg) {
         ATTN_TR(10, gg);
+        const uint32_t stv = pv_next % NV, phv = (pv_next / NV) & 1;
         mbar_wait(p_full, gg & 1);
         mbar_wait(&full_v[stv], phv);
         tc_after();
-        const uint32_t v_sub = D < 64 ? ((a.pieces[v_pc].head * D) & 63u) * 2 : 0;
+        const uint32_t v_sub = D < 64 ? ((a.pieces[pv_pc].head * D) & 63u) * 2 : 0;
         const uint64_t bv = dv0 + ((stv * T_BYTES + v_sub) >> 4);
         const uint32_t a_tmem = tmem + C::S_COL + (gg & 1) * BN;  // P(gg) over S(gg)'s buffer
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
           mma_ts_if(leader, tmem + C::O_COL, a_tmem + kk * 8, bv + ((kk * 2048) >> 4), idesc_o,
                     (v_j > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_ts_if(leader, tmem + C::L_COL, a_tmem + kk * 8, d_ones, idesc_l, (v_j > 0 || kk > 0) ? 1u : 0u);
         mma_commit_if(leader, o_done);
+        mma_commit_if(leader, &empty_v[stv]);  // V stage read once PV completed
         if (leader) ATTN_TR(2, gg);
-        if (++stv == NV) { stv = 0; phv ^= 1; }
+        ++pv_next;
         ++v_j;
-        if (--v_left == 0) {
-          ++v_pc;
+        if (--pv_left == 0) {
+          ++pv_pc;
           v_j = 0;
-          if (v_pc < pe) { const AttnPiece Pn = a.pieces[v_pc]; v_left = Pn.hi - Pn.lo; }
+          ++pv_next;  // skip the next piece's Q
+          if (pv_pc < pe) { const AttnPiece Pn = a.pieces[pv_pc]; pv_left = Pn.hi - Pn.lo; }
         }
         if (s_g < total) issue_s();
       }
@@ -542,25 +572,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_base = (32u * (warp % 4)) << 16;
     const uint32_t o_col = tmem + lane_base + C::O_COL + wg * (D / 2);
     uint32_t t_all = 0;      // tiles processed (barrier phases)
-    int32_t pend_v = -1;     // tile whose V stage this warp still has to release
-    uint32_t stk = 0;        // K stage of the current tile
-    auto release_v = [&]() {
-      if (pend_v >= 0) {
-        if (lane == 0) mbar_arrive(&empty_v[uint32_t(pend_v) % NV]);
-        pend_v = -1;
-      }
-    };
     auto named_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
-    int32_t epi_pending = -1;  // piece whose staged partial tiles may still be read by TMA stores
-    auto flush_epi = [&]() {   // hand the staging (Q) buffer back once the stores have read it
-      if (epi_pending >= 0) {
-        if (lane == 0) {
-          bulk_wait_read<0>();
-          mbar_arrive(&epi_done[uint32_t(epi_pending) & 1]);
-        }
-        epi_pending = -1;
-      }
-    };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const uint64_t KA = P.start + P.n_hist;
@@ -579,7 +591,7 @@ __global__ void __launch_bounds__(384, 1)
       const int64_t span = int64_t(P.hi - P.lo) * BN;
       auto rel = [&](uint64_t x) { return int(min(max(int64_t(x) - int64_t(kb0), int64_t(-1)), span)); };
       const int ue = rel(u_end), cl = rel(KAp), ce = rel(c_end);
-      float m_ref = -INFINITY, l_part = 0.f;
+      float m_ref = -INFINITY;
       for (uint32_t t = P.lo; t < P.hi; ++t, ++t_all) {
         const uint32_t b = t_all & 1;
         mbar_wait(&s_full[b], (t_all >> 1) & 1);
@@ -589,10 +601,6 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int c = 0; c < HC / 32; ++c) tmem_ld32(tmem + lane_base + C::S_COL + b * BN + wg * HC + c * 32, s + c * 32);
         tmem_wait_ld();
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_k[stk]);
-        if (++stk == NK) stk = 0;
         const int kb = int(t - P.lo) * BN;
         const int cu = min(max(ue - kb, 0), HC), c_lo = min(max(cl - kb, 0), HC), c_hi = min(max(ce - kb, 0), HC);
         if (cu != HC) {
@@ -617,14 +625,12 @@ __global__ void __launch_bounds__(384, 1)
           m_ref = mx;
         }
         const float nmref = m_ref == -INFINITY ? 0.f : -m_ref;
-        float r4[4] = {0.f, 0.f, 0.f, 0.f};
+        // (the row sum of P is accumulated by the tensor core: L += P x ones)
 #pragma unroll
         for (int c = 0; c < HC; ++c) {
           const float x = fmaf(s[c], a.scale_log2, nmref);
           s[c] = (POLY && c % POLY == POLY - 1) ? ex2_poly(x) : ex2(x);
-          r4[c & 3] += s[c];
         }
-        l_part = l_part * alpha + ((r4[0] + r4[1]) + (r4[2] + r4[3]));
         if (threadIdx.x % 128 == 0) ATTN_TR(7, t_all);
         // P over the first BN/2 columns of this S buffer (this half's HC/2 columns)
 #pragma unroll
@@ -637,8 +643,8 @@ __global__ void __launch_bounds__(384, 1)
         if (t != P.lo) {  // the previous PV must finish before O is rescaled
           mbar_wait(o_done, (t_all - 1) & 1);
           tc_after();
-          release_v();
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            if (wg == 0) tmem_st1(tmem + lane_base + C::L_COL, tmem_ld1(tmem + lane_base + C::L_COL) * alpha);
             if constexpr (D >= 64) {
 #pragma unroll 1
               for (int c = 0; c < D / 64; ++c) {
@@ -665,8 +671,6 @@ __global__ void __launch_bounds__(384, 1)
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
-        pend_v = int32_t(t_all);
-        flush_epi();
         if (threadIdx.x % 128 == 0) ATTN_TR(4, t_all);
       }
       // ---- epilogue: O / l and lse (base 2) into slot `part` ----
@@ -674,90 +678,43 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t qi = q0 + r;
       mbar_wait(o_done, (t_all - 1) & 1);
       tc_after();
-      release_v();
       if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb));
-      float* l_buf = sMax + (t_all & 1) * 2 * BM;  // the buffer the next tile's max exchange will use
-      l_buf[wg * BM + r] = l_part;
-      named_sync();
-      const float l_run = l_buf[r] + l_buf[BM + r];
-      named_sync();  // both halves read l before the buffer is reused
+      const float l_run = tmem_ld1(tmem + lane_base + C::L_COL);  // row sum of P (all 16 columns equal)
+      tmem_wait_ld();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb) + 1);
+      // O/l straight from TMEM to the slot: thread r owns row r's D/2 columns of
+      // this half; in the chunked slot layout (part_index) a warp's store of
+      // one 4-column chunk covers 32 consecutive rows = 512 contiguous bytes.
+      // Rows past the tile's valid rows are not written (the combine never
+      // reads them).
       {
-        // O/l -> HBM through a per-warp staging tile in this piece's (already
-        // copied) Q buffer: tcgen05.ld gives one row per thread, the staged
-        // tile is written back as whole 128-B row segments (coalesced)
-        constexpr int CW = D / 4;                 // staged columns per pass (8 warps x 32 rows x CW fp32 = Q_BYTES)
-        constexpr int C4 = CW / 4;
-        // the tcgen05.cp that read this Q buffer completed before this piece's first
-        // S (the s_full commits track all earlier tcgen05 operations)
-        const uint32_t qb = (pc - pb) & 1;
-        float* stg = reinterpret_cast<float*>(sQ + qb * Q_BYTES) + (warp - 4) * 32 * CW;
-        const uint32_t row0 = (warp % 4) * 32;    // first TMEM lane (query row) of this warp
-        if constexpr (CW == 32) {
-          // D = 128: the warp's 64 O columns leave in four 32-row x 16-column fp32
-          // tiles through TMA bulk tensor stores, alternating between two 2 KB
-          // halves of its staging area, so no pass waits on HBM writes; rows past
-          // the query tile's valid rows land in unused rows of the slot
-          constexpr int PW = 16;  // columns per pass
+        constexpr int CW = D / 2 >= 32 ? 32 : D / 2;  // columns per tcgen05.ld
+        float* dst = a.part_o + part_index(P.part, BM, r, wg * (D / 2), D);
+        constexpr size_t chunk_stride = size_t(BM) * 4;  // floats between consecutive 4-column chunks
+        const bool valid = qi < q_end;
 #pragma unroll 1
-          for (int c = 0; c < D / 2 / PW; ++c) {
-            float* half = stg + (c & 1) * 32 * PW;
-            if (c >= 2) {
-              if (lane == 0) bulk_wait_read<1>();  // the store that used this half has read it
-              __syncwarp();
-            }
-            float o[16];
-            tmem_ld16(o_col + c * PW, o);
-            tmem_wait_ld();
-            // 64-B swizzled rows (the part map's SWIZZLE_64B): 16-B chunk k of row
-            // `lane` sits at chunk k ^ ((lane >> 1) & 3) — conflict-free stores
+        for (int c = 0; c < D / 2 / CW; ++c) {
+          float o[CW];
+          if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
+          else tmem_ld16(o_col + c * CW, o);
+          tmem_wait_ld();
+          if (valid) {
 #pragma unroll
-            for (int k = 0; k < PW / 4; ++k)
-              *reinterpret_cast<float4*>(half + lane * PW + 4 * (k ^ ((lane >> 1) & 3))) =
+            for (int k = 0; k < CW / 4; ++k)
+              *reinterpret_cast<float4*>(dst + (c * CW / 4 + k) * chunk_stride) =
                   make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&part_map, half, int(wg * (D / 2) + c * PW), int(P.part * BM + row0));
-              bulk_commit();
-            }
-            if (threadIdx.x == 128 && c < 2) ATTN_TR(11, 4 * (pc - pb) + 2 + c);
-          }
-          epi_pending = int32_t(pc - pb);  // epi_done is signalled once the stores have read the staging
-        } else {
-          float* dst_slot = a.part_o + size_t(P.part) * BM * D + wg * (D / 2);
-#pragma unroll 1
-          for (int c = 0; c < D / 2 / CW; ++c) {
-            float o[32];
-            tmem_ld16(o_col + c * CW, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < C4; ++k)
-              *reinterpret_cast<float4*>(stg + lane * CW + ((k ^ (lane % C4)) << 2)) =
-                  make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
-            __syncwarp();
-#pragma unroll
-            for (int it = 0; it < C4; ++it) {
-              const uint32_t qd = lane + 32 * it, rr = qd / C4, k = qd % C4;
-              const float4 v = *reinterpret_cast<const float4*>(stg + rr * CW + ((k ^ (rr % C4)) << 2));
-              if (q0 + row0 + rr < q_end)
-                *reinterpret_cast<float4*>(dst_slot + size_t(row0 + rr) * D + c * CW + 4 * k) = v;
-            }
-            __syncwarp();
           }
         }
       }
       const size_t prow = size_t(P.part) * BM + r;
       if (wg == 0 && qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
       if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
+      // O is overwritten by the next piece's first PV (issued after p_full of
+      // its first tile, which this thread signals after the loads above)
       tc_before();
-      __syncwarp();
-      if (epi_pending < 0 && lane == 0) mbar_arrive(&epi_done[(pc - pb) & 1]);
     }
     if (threadIdx.x == 128) ATTN_TR(5, 2);
-    flush_epi();
-    if (lane == 0) bulk_wait_all();  // the partial tiles are in global memory before the CTA retires
   }
   tc_before();
   __syncthreads();
@@ -806,28 +763,13 @@ int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g) {
   return encode_2d(map, pool, g.d, uint64_t(g.L) * g.num_pages * 2 * g.S, g.S);
 }
 
-// partial O slots [slots * 128 rows][D] fp32, box = 16 cols x 32 rows, no swizzle
-// (the attention epilogue's staged tiles; D = 128; 64-B rows, 64-B swizzle)
-int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t D) {
-  const cuuint64_t dims[2] = {D, rows};
-  const cuuint64_t strides[1] = {cuuint64_t(D) * 4};
-  const cuuint32_t box[2] = {16, 32};
-  const cuuint32_t estr[2] = {1, 1};
-  auto fn = encode_fn();
-  if (!fn) return -1;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(part_o), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : -2;
-}
-
 // fresh-row queries [rows][d], box = 64 cols x 128 rows (rows past the buffer load as zeros)
 int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g) {
   return encode_2d(map, q, g.d, rows, BM);
 }
 
 template <int D, bool TR, int POLY>
-static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map,
                        const AttnArgs& a, cudaStream_t s) {
   static DeviceOnce once;
   if (once.first())
@@ -842,23 +784,25 @@ static void launch_cfg(const CUtensorMap& pool_map, const CUtensorMap& q_map, co
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, TR, POLY>, pool_map, q_map, part_map, a);
+  cudaLaunchKernelEx(&cfg, attn_tc_kernel<D, TR, POLY>, pool_map, q_map, a);
 }
 
 template <int D>
-static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+static void launch_tc_d(const CUtensorMap& pool_map, const CUtensorMap& q_map,
                         const AttnArgs& a, cudaStream_t s) {
   static const int poly = [] {
     const char* e = std::getenv("MTKV_ATTN_POLY");
     return e ? std::atoi(e) : kPolyDefault;
   }();
-  if (a.trace) launch_cfg<D, true, kPolyDefault>(pool_map, q_map, part_map, a, s);
-  else if (poly == 4) launch_cfg<D, false, 4>(pool_map, q_map, part_map, a, s);
-  else if (poly == 8) launch_cfg<D, false, 8>(pool_map, q_map, part_map, a, s);
-  else launch_cfg<D, false, 0>(pool_map, q_map, part_map, a, s);
+  if (a.trace) launch_cfg<D, true, kPolyDefault>(pool_map, q_map, a, s);
+  else if (poly == 2) launch_cfg<D, false, 2>(pool_map, q_map, a, s);
+  else if (poly == 3) launch_cfg<D, false, 3>(pool_map, q_map, a, s);
+  else if (poly == 4) launch_cfg<D, false, 4>(pool_map, q_map, a, s);
+  else if (poly == 8) launch_cfg<D, false, 8>(pool_map, q_map, a, s);
+  else launch_cfg<D, false, 0>(pool_map, q_map, a, s);
 }
 
-void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map,
                          const AttnArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
   static const bool no_trigger = [] {  // MTKV_ATTN_TRIGGER=0: A/B switch for the early PDL release
@@ -867,9 +811,9 @@ void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, 
   }();
   AttnArgs b = a;
   if (no_trigger) b.trigger = 0;
-  if (a.g.D == 32) launch_tc_d<32>(pool_map, q_map, part_map, b, s);
-  else if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, part_map, b, s);
-  else launch_tc_d<128>(pool_map, q_map, part_map, b, s);
+  if (a.g.D == 32) launch_tc_d<32>(pool_map, q_map, b, s);
+  else if (a.g.D == 64) launch_tc_d<64>(pool_map, q_map, b, s);
+  else launch_tc_d<128>(pool_map, q_map, b, s);
 }
 
 }  // namespace mtkv_b200

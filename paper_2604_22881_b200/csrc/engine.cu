@@ -106,6 +106,8 @@ Engine::~Engine() {
       cudaEventDestroy(ev_onload_[k]); cudaEventDestroy(ev_scatter_[k]);
       cudaEventDestroy(ev_gathered_[k]); cudaEventDestroy(ev_d2h_[k]);
       cudaEventDestroy(ev_done_[k]); cudaEventDestroy(ev_start_[k]); cudaEventDestroy(ev_meta_[k]);
+      cudaEventDestroy(ev_stk0_[k]); cudaEventDestroy(ev_stk1_[k]); cudaEventDestroy(ev_h2d0_[k]);
+      cudaEventDestroy(ev_h2d1_[k]);
     }
     for (auto e : ev_attn_) cudaEventDestroy(e);
     for (auto e : ev_copy_)
@@ -196,6 +198,10 @@ int Engine::init(std::string& err) {
     CK(cudaEventCreate(&ev_done_[k]));
     CK(cudaEventCreate(&ev_start_[k]));
     CK(cudaEventCreateWithFlags(&ev_meta_[k], cudaEventDisableTiming));
+    CK(cudaEventCreate(&ev_stk0_[k]));
+    CK(cudaEventCreate(&ev_stk1_[k]));
+    CK(cudaEventCreate(&ev_h2d0_[k]));
+    CK(cudaEventCreate(&ev_h2d1_[k]));
   }
   if (!recompute_) {
     if (pool_.ensure(size_t(g_.L) * g_.num_pages * 2 * g_.S * g_.d * sizeof(__nv_bfloat16))) {
@@ -393,7 +399,36 @@ int Engine::set_onload_policy(uint32_t policy, double gbs, double mtok_s, std::s
   const double d = g_.d, flops = double(g_.L) * (12.0 * d * d + 2.0 * 2.0 * 2048.0 * d);
   const double tps = mtok_s > 0 ? mtok_s * 1e6 : 2e14 / flops;
   planner.set_onload_policy(int(policy), (gbs > 0 ? gbs : 54.0) * 1e9, tps);
+  // no rate given: the value engine measures both (calibrate_from) and the
+  // policy follows the measured rates; the tag backend has no layer stack to time
+  calibrate_ = value_ && policy == MTKV_ONLOAD_ADAPTIVE && mtok_s <= 0;
+  cal_tps_ = cal_Bps_ = 0;
+  for (int k = 0; k < kRing; ++k) cal_rows_[k] = cal_bytes_[k] = 0;
   return MTKV_OK;
+}
+
+// Adaptive policy calibration from a completed batch (ring slot k): the layer
+// stack's rows per second on the SMs and the onload bytes per second over the
+// host link, as exponential moving averages. The policy balances the two per
+// batch, so its rates must be this box's, not a model's: at d = 256 the stack
+// runs ~2.5x faster than the FLOP estimate (its attention is softmax-bound,
+// not FLOP-bound). Changes only which host hits are re-encoded instead of
+// onloaded; the control plane never sees it.
+void Engine::calibrate_from(int k) {
+  if (!calibrate_) return;
+  constexpr double a = 0.25;
+  float ms = 0;
+  if (cal_rows_[k] >= 4096 && cudaEventElapsedTime(&ms, ev_stk0_[k], ev_stk1_[k]) == cudaSuccess && ms > 0) {
+    const double tps = double(cal_rows_[k]) / (ms * 1e-3);
+    cal_tps_ = cal_tps_ > 0 ? (1 - a) * cal_tps_ + a * tps : tps;
+  }
+  if (cal_bytes_[k] >= (size_t(8) << 20) && cudaEventElapsedTime(&ms, ev_h2d0_[k], ev_h2d1_[k]) == cudaSuccess && ms > 0) {
+    const double bps = double(cal_bytes_[k]) / (ms * 1e-3);
+    cal_Bps_ = cal_Bps_ > 0 ? (1 - a) * cal_Bps_ + a * bps : bps;
+  }
+  cal_rows_[k] = cal_bytes_[k] = 0;
+  (void)cudaGetLastError();  // an unavailable timing is skipped, not an engine error
+  if (cal_tps_ > 0 && cal_Bps_ > 0) planner.set_onload_policy(int(opt_.onload_policy), cal_Bps_, cal_tps_);
 }
 
 int Engine::process_batch(const mtkv_request* reqs, uint32_t n, std::string& err) {
@@ -427,6 +462,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     CK(cudaEventSynchronize(ev_done_[k]));
     if (d2h_rec_batch_[k] >= 0) CK(cudaEventSynchronize(ev_d2h_[k]));
     d2h_done_upto_ = int64_t(batch_no_) - kRing;
+    calibrate_from(k);
   }
 
   const uint32_t S = g_.S, d = g_.d, H = g_.H, V = value_ ? opt_.model.vocab : 0;
@@ -451,6 +487,9 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
         err = "engine: cannot grow the transient page pool";
         return MTKV_ERROR;
       }
+      // fresh allocation bits may be NaN patterns: page padding and unused
+      // candidate slots are read with P = 0, and 0 x NaN poisons O
+      CK(cudaMemsetAsync(pool_.p, 0, pool_.bytes, comp_));
     }
   }
   const std::vector<uint32_t>& pages = recompute_ ? tpages : w.pages;
@@ -607,6 +646,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       return MTKV_ERROR;
     }
     if (batch_no_ >= 2) CK(cudaStreamWaitEvent(h2d_, ev_scatter_[(batch_no_ - 2) % kRing], 0));
+    if (calibrate_) {
+      CK(cudaEventRecord(ev_h2d0_[k], h2d_));
+      cal_bytes_[k] = uint64_t(n_on) * chunk_bytes_;
+    }
     int64_t waited = -1;
     for (uint32_t j = 0; j < n_on;) {
       // a run of chunks contiguous in the host extent -> one transfer into
@@ -637,6 +680,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       j += run;
     }
     CK(cudaEventRecord(ev_onload_[k], h2d_));
+    if (calibrate_) CK(cudaEventRecord(ev_h2d1_[k], h2d_));
     h2d_bytes_ += uint64_t(n_on) * chunk_bytes_;
     onload_chunks_ += n_on;
   }
@@ -678,7 +722,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     const size_t rb = size_t(rows) * d * sizeof(__nv_bfloat16);
     // comp-only workspaces: stream-ordered growth (no device synchronisation)
     if (x_.ensure(rb, comp_) || x2_.ensure(rb, comp_) || u_.ensure(rb, comp_) || q_.ensure(rb, comp_) ||
-        mid_.ensure(rb, comp_) || part_o_.ensure(size_t(plan_.n_slots) * bq * g_.D * sizeof(float), comp_) ||
+        mid_.ensure(rb, comp_) || part_o_.ensure(size_t(plan_.n_slots) * part_slot_floats(bq, g_.D) * sizeof(float), comp_) ||
         part_lse_.ensure(size_t(plan_.n_slots) * bq * sizeof(float), comp_) ||
         logits_.ensure(size_t(n) * V * sizeof(float), comp_) ||
         scores_.ensure(size_t(ncand_total) * sizeof(float), comp_)) {
@@ -690,6 +734,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     auto* U = static_cast<__nv_bfloat16*>(u_.p);
     auto* Q = static_cast<__nv_bfloat16*>(q_.p);
     auto* MID = static_cast<__nv_bfloat16*>(mid_.p);
+    if (calibrate_) {
+      CK(cudaEventRecord(ev_stk0_[k], comp_));
+      cal_rows_[k] = rows;
+    }
     launch_embed(X, w_embed_, d_tok, rows, d, comp_);
     ++launches;
     const bool prof = opt_.profile != 0;
@@ -741,15 +789,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
           q_map_ptr_ = q_.p;
           q_map_bytes_ = q_.bytes;
         }
-        if (part_map_ptr_ != part_o_.p || part_map_bytes_ != part_o_.bytes) {
-          if (make_part_map(&part_map_, part_o_.p, part_o_.bytes / (size_t(g_.D) * sizeof(float)), g_.D)) {
-            err = "engine: cuTensorMapEncodeTiled (attention partials) failed";
-            return MTKV_ERROR;
-          }
-          part_map_ptr_ = part_o_.p;
-          part_map_bytes_ = part_o_.bytes;
-        }
-        launch_attention_tc(pool_map_, q_map_, part_map_, aa, comp_);
+        launch_attention_tc(pool_map_, q_map_, aa, comp_);
       } else {
         launch_attention(aa, comp_);
       }
@@ -776,6 +816,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
           static_cast<float*>(scores_.p), static_cast<const float*>(logits_.p), d_creq, d_cid, ncand_total, V);
       ++launches;
     }
+    if (calibrate_) CK(cudaEventRecord(ev_stk1_[k], comp_));
   } else {
     launch_tag_append(pool, d_req, d_pages, n, max_hist, g_, comp_);
     ++launches;

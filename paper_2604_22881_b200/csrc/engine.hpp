@@ -94,6 +94,14 @@ class Engine {
   cudaStream_t comp_ = nullptr, h2d_ = nullptr, d2h_ = nullptr;
   cudaEvent_t ev_onload_[kRing], ev_scatter_[kRing], ev_gathered_[kRing], ev_d2h_[kRing],
       ev_done_[kRing], ev_start_[kRing], ev_meta_[kRing];
+  // adaptive-policy calibration: per ring slot, the layer stack's span on comp
+  // (embed -> scores) and the onload copies' span on h2d, with the rows / bytes
+  // they processed; read back when the slot is reused (the batch is complete)
+  cudaEvent_t ev_stk0_[kRing], ev_stk1_[kRing], ev_h2d0_[kRing], ev_h2d1_[kRing];
+  uint64_t cal_rows_[kRing] = {0, 0, 0, 0}, cal_bytes_[kRing] = {0, 0, 0, 0};
+  double cal_tps_ = 0, cal_Bps_ = 0;  // EMAs (0: no measurement yet)
+  bool calibrate_ = false;            // adaptive policy with no fixed rates given
+  void calibrate_from(int k);
   std::vector<cudaEvent_t> ev_attn_;  // profiling pairs of the last batch
   cudaEvent_t ev_copy_[4] = {nullptr, nullptr, nullptr, nullptr};  // scatter start/end, gather start/end
   uint32_t prof_scatter_ = 0, prof_gather_ = 0;
@@ -123,9 +131,6 @@ class Engine {
   uint32_t pool_map_pages_ = 0;
   const void* q_map_ptr_ = nullptr;
   size_t q_map_bytes_ = 0;
-  alignas(64) CUtensorMap part_map_{};
-  const void* part_map_ptr_ = nullptr;
-  size_t part_map_bytes_ = 0;
 
   // pinned host memory: slabs -> per-user extents -> chunks
   static constexpr size_t kSpareSlabs = 2;

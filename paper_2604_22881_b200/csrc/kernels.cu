@@ -410,14 +410,14 @@ __global__ void __launch_bounds__(NW * 32) attn_kernel(AttnArgs a) {
     const uint32_t qi = q0 + warp * 16 + gq + r * 8;
     if (qi >= q_end) continue;
     const AttnSeg& sg = a.segs[R.seg0 + h * R.qtiles + it.qtile];
-    const size_t prow = (size_t)(sg.part_base + it.split) * ABQ + (qi - q0);
+    const uint32_t slot = sg.part_base + it.split;
+    const size_t prow = (size_t)slot * ABQ + (qi - q0);
     const float inv = l_r[r] > 0.f ? 1.f / l_r[r] : 0.f;
-    float* dst = a.part_o + prow * D;
 #pragma unroll
     for (int i = 0; i < NDT; ++i) {
       const uint32_t col = i * 8 + tq * 2;
-      if (col < D) dst[col] = o[i][r * 2] * inv;
-      if (col + 1 < D) dst[col + 1] = o[i][r * 2 + 1] * inv;
+      if (col < D) a.part_o[part_index(slot, ABQ, qi - q0, col, D)] = o[i][r * 2] * inv;
+      if (col + 1 < D) a.part_o[part_index(slot, ABQ, qi - q0, col + 1, D)] = o[i][r * 2 + 1] * inv;
     }
     if (tq == 0) a.part_lse[prow] = l_r[r] > 0.f ? m_r[r] + log2f(l_r[r]) : -INFINITY;
   }
@@ -465,7 +465,7 @@ __device__ __forceinline__ float gate_merge_col(const GateArgs& a, const AttnSeg
     const float l = a.part_lse[prow];
     if (l == -INFINITY) continue;
     const float w = exp2f(l - mx);
-    num += w * a.part_o[prow * a.D + c];
+    num += w * a.part_o[part_index(sg.part_base + k, a.bm, ri, c, a.D)];
     den += w;
   }
   return den > 0.f ? num / den : 0.f;
@@ -521,16 +521,15 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
       if (l == -INFINITY) continue;
       const float w = exp2f(l - mx);
       den += w;
-      const float* src = a.part_o + prow * a.D + c0;
-      if constexpr (E % 4 == 0) {
+      if constexpr (E % 4 == 0) {  // c0 % 4 == 0: every 4 columns are one chunk of the slot
 #pragma unroll
         for (int e = 0; e < E; e += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(src + e);
+          const float4 v = *reinterpret_cast<const float4*>(a.part_o + part_index(sg.part_base + k, a.bm, ri, c0 + e, a.D));
           acc[e] += w * v.x; acc[e + 1] += w * v.y; acc[e + 2] += w * v.z; acc[e + 3] += w * v.w;
         }
       } else {
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc[e] += w * src[e];
+        for (int e = 0; e < E; ++e) acc[e] += w * a.part_o[part_index(sg.part_base + k, a.bm, ri, c0 + e, a.D)];
       }
     }
     const float inv = den > 0.f ? 1.f / den : 0.f;

@@ -100,6 +100,17 @@ int launch_gemm_tc(const GemmArgs& a, uint64_t a_rows_alloc, cudaStream_t s);
 void launch_embed(__nv_bfloat16* x, const __nv_bfloat16* table, const uint32_t* tok, int rows, int d,
                   cudaStream_t s);
 
+// Partial-O slot layout (attention -> combine): per slot, 4-column chunks of
+// all bm rows are contiguous ([slot][D/4 chunks][bm rows][4]). Thread r of the
+// tcgen05 epilogue owns query row r, so a warp's 16-B stores of one chunk are
+// 32 consecutive rows = 512 contiguous bytes (row-major slots made every
+// store instruction touch 32 rows).
+__host__ __device__ inline uint32_t part_chunks(uint32_t D) { return (D + 3) / 4; }
+__host__ __device__ inline size_t part_index(uint32_t slot, uint32_t bm, uint32_t ri, uint32_t c, uint32_t D) {
+  return ((size_t(slot) * part_chunks(D) + c / 4) * bm + ri) * 4 + (c & 3);
+}
+__host__ __device__ inline size_t part_slot_floats(uint32_t bm, uint32_t D) { return size_t(part_chunks(D)) * 4 * bm; }
+
 struct AttnArgs {
   const __nv_bfloat16* q;   // [rows x d]
   const __nv_bfloat16* pool;
@@ -110,7 +121,7 @@ struct AttnArgs {
   uint32_t n_items;         // mma.sync path: CTAs; tcgen05 path: persistent CTAs
   const AttnPiece* pieces;  // tcgen05 path: pieces of CTA c = [cta_off[c], cta_off[c+1])
   const uint32_t* cta_off;
-  float* part_o;            // [slots x bm x D]
+  float* part_o;            // [slots][D/4][bm][4] (part_index)
   float* part_lse;          // [slots x bm]
   PoolGeom g;
   uint32_t layer;
@@ -164,8 +175,7 @@ namespace mtkv_b200 {
 bool attn_tc_supported(const PoolGeom& g);
 int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g);
 int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g);
-int make_part_map(CUtensorMap* map, const void* part_o, uint64_t rows, uint32_t D);
-void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map, const CUtensorMap& part_map,
+void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map,
                          const AttnArgs& a, cudaStream_t s);
 int num_sms();
 

@@ -79,7 +79,7 @@ __global__ void merge_segs_kernel(float* out, const float* part, const float* ls
     const size_t prow = size_t(sg.part_base + k) * bm + ri;
     if (lse[prow] == -INFINITY) continue;
     const float w = exp2f(lse[prow] - m);
-    num += w * part[prow * D + c];
+    num += w * part[part_index(sg.part_base + k, bm, ri, c, D)];
     den += w;
   }
   out[idx] = den > 0.f ? num / den : 0.f;
@@ -125,7 +125,7 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
   const size_t o_pieces = carve(plan.pieces.size() * sizeof(AttnPiece));
   const size_t o_cta = carve(plan.cta_off.size() * sizeof(uint32_t));
   const size_t o_lse = carve(size_t(plan.n_slots) * plan.bm * sizeof(float));
-  const size_t o_part = carve(size_t(plan.n_slots) * plan.bm * g.D * sizeof(float));
+  const size_t o_part = carve(size_t(plan.n_slots) * part_slot_floats(plan.bm, g.D) * sizeof(float));
   char* buf = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&buf, off, s);
   if (e != cudaSuccess) return finish(e);
@@ -156,9 +156,8 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
   a.bq = plan.bm;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
   if (e == cudaSuccess) {
-    alignas(64) CUtensorMap pmap, qmap, omap;
-    if (tc && (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, rows, g) ||
-               make_part_map(&omap, a.part_o, uint64_t(plan.n_slots) * plan.bm, g.D))) {
+    alignas(64) CUtensorMap pmap, qmap;
+    if (tc && (make_pool_map(&pmap, pool, g) || make_q_map(&qmap, q, rows, g))) {
       cudaFreeAsync(buf, s);
       set_last_error("paged_attention: cuTensorMapEncodeTiled failed");
       return MTKV_ERROR;
@@ -186,7 +185,7 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
         cudaMemsetAsync(flush, int(it & 0xFF), size_t(256) << 20, s);
         cudaEventRecord(ev[2 * (it - 1)], s);
       }
-      if (tc) launch_attention_tc(pmap, qmap, omap, a, s);
+      if (tc) launch_attention_tc(pmap, qmap, a, s);
       else launch_attention(a, s);
       if (it >= 1 && !ev.empty()) cudaEventRecord(ev[2 * (it - 1) + 1], s);
     }

@@ -14,9 +14,13 @@
   (+ recomputed lost tail) -> revisit, in all three modes, every request's
   logits against the fp64 restatement of the reference model
   (tests/ref_model.py, pinned to the reference): per request max|dlogit| <=
-  LOGIT_REL x max|ref logit|; and the modes against each other <= MODE_REL
-  (the reference's acceptance criterion 2, tests/acceptance.cpp:104, requires
-  mode-invariant logits; here within bf16 storage / fp32 accumulation).
+  LOGIT_REL x max|ref logit|; resident K/V per (user, layer) <= KV_REL x
+  max|ref K/V|; and the modes against each other <= MODE_REL (K/V) /
+  MODE_REL_LOGIT (logits) (the reference's acceptance criterion 2,
+  tests/acceptance.cpp:104, requires mode-invariant logits; here within bf16
+  storage / fp32 accumulation). At L = 4 the reference model's logits are
+  ~1e-44 (below fp32's normal range), so L = 4 checks the K/V and L = 3 the
+  logits (see the test's docstring).
 """
 import numpy as np
 import pytest
@@ -30,7 +34,9 @@ pytestmark = pytest.mark.gpu
 
 ATTN_REL = 1e-2
 LOGIT_REL = 0.03
-MODE_REL = 1e-2
+KV_REL = 0.03
+MODE_REL = 1e-2        # modes against each other: K/V in the pool
+MODE_REL_LOGIT = 2e-2  # and logits (bf16 roundings of differently materialised prefixes compound per layer)
 POISON_K, POISON_V = 30.0, 1000.0
 
 
@@ -144,43 +150,93 @@ def _configs1_trace(users=32, history=4096, delta=64, cands=8, vocab=4096, round
     return tr
 
 
-def test_value_engine_configs1_dims_evict_onload_all_modes_vs_fp64():
-    L, H, D, V = 4, 2, 128, 4096
+def _bits_f32(a):
+    return (np.asarray(a, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("L", [4, 3])
+def test_value_engine_configs1_dims_evict_onload_all_modes_vs_fp64(L):
+    """configs[1] widths (d=256, H=2, D=128, vocab 4096, 4K-token prefixes) through
+    prefill -> eviction -> host onload (+ recomputed lost tail) -> revisit.
+
+    L = 4 (the bench depth): the reference model (model.cpp:34, init scale
+    0.3/sqrt(d), no residual path, layer-norm eps 1e-6) shrinks each layer's
+    activations by ~1e-8 once the 4K-key attention averages the values, so its
+    4-layer logits are ~1e-44 in fp64 -- below fp32's normal range; no fp32
+    engine can represent them. At L = 4 the check is therefore the K/V every
+    layer appended / onloaded into the pool (the data the cache serves; layer 3
+    K/V are ~1e-20, representable), per (user, layer) against the fp64 K/V.
+    L = 3 (logits ~1e-24): per-request logits against fp64, plus the K/V.
+    Both: the modes against each other (acceptance.cpp:104 criterion 2)."""
+    H, D, V = 2, 128, 4096
     # pool ~17 users of 32: revisits in a random order miss about half the time;
     # locked (offloading) users hold at most the quota's worth of pages, so a
     # batch of 8 always finds victims
-    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=32, chunk_size=128, device_pages=2400,
-                  offload_quota=128 * 64 * 4))
+    kv = _kv(dict(num_layers=L, num_heads=H, head_dim=D, page_size=32, chunk_size=128,
+                  device_pages=2400 * L // 4, offload_quota=128 * 64 * 4))
     mc = mtkv.ModelConfig(num_layers=L, num_heads=H, head_dim=D, vocab=V, seed=1)
     trace = _configs1_trace(vocab=V)
     srv = RefServer(RefModel(ModelParams(num_layers=L, num_heads=H, head_dim=D, vocab=V, seed=1), device="cuda"))
-    ref = [srv.serve(r["user"], r["tokens"], r["cands"]).cpu().numpy() for r in trace]
     bs_of = lambda i: 4 if i < 32 else 8
-    got = {}
+    ref, ref_kv, i = [], [], 0
+    while i < len(trace):  # fp64 logits of every request, and the K/V each batch's users hold after it
+        b = trace[i:i + bs_of(i)]
+        ref.extend(srv.serve(r["user"], r["tokens"], r["cands"]).cpu().numpy() for r in b)
+        ref_kv.append({r["user"]: ([k.float().cpu().numpy() for k in srv.k[r["user"]]],
+                                   [v.float().cpu().numpy() for v in srv.v[r["user"]]]) for r in b})
+        i += len(b)
+    check_logits = L <= 3
+    if check_logits:
+        assert min(np.abs(r).max() for r in ref) > 1e-30  # fp32-representable
+    got, got_kv = {}, {}
     for mode in ("hierarchical", "hierarchical+adaptive", "gpu_only", "recompute"):
         m, _, pol = mode.partition("+")
         eng = mtkv.Engine(kv, mode=m, backend="value", batch_size=8, model=mc, keep_logits=True,
                           onload_policy=pol or "always", recompute_mtok_s=30.0)
-        out, i = [], 0
+        out, kv_err, kv_last, i, bi = [], [], {}, 0, 0
         while i < len(trace):
             b = trace[i:i + bs_of(i)]
             eng.process_batch(b)
             out.extend(np.asarray(eng.last_logits(), dtype=np.float64))
+            eng.synchronize()
+            for u, (rk, rv) in (ref_kv[bi].items() if m != "recompute" else ()):  # recompute caches nothing
+                n = eng.user_state(u)["device_len"]
+                assert n == rk[0].shape[0], (mode, u, n)  # the served user's whole history is resident
+                for layer in range(L):
+                    k, v = eng.read_user_kv(u, layer)
+                    kf, vf = _bits_f32(k), _bits_f32(v)
+                    for g_, r_ in ((kf, rk[layer]), (vf, rv[layer])):
+                        kv_err.append(float(np.abs(g_ - r_).max() / np.abs(r_).max()))
+                    kv_last[(u, layer)] = (kf, vf)
             i += len(b)
+            bi += 1
         rep = eng.report()
-        rel = np.array([np.abs(g - r).max() / np.abs(r).max() for g, r in zip(out, ref)])
-        ab = np.array([np.abs(g - r).max() for g, r in zip(out, ref)])
-        print(f"{mode}: {len(out)} requests, evictions {rep['evictions']}, host-onloaded tokens "
-              f"{rep['hist_host']}, per-request rel err max {rel.max():.3e} mean {rel.mean():.3e} "
-              f"(revisits max {rel[32:].max():.3e}), abs err max {ab.max():.3e}")
+        kv_err = np.array(kv_err or [0.0])
+        msg = (f"L={L} {mode}: {len(out)} requests, evictions {rep['evictions']}, host-onloaded tokens "
+               f"{rep['hist_host']}, K/V per (user, layer) rel err max {kv_err.max():.3e} mean {kv_err.mean():.3e}")
+        if check_logits:
+            rel = np.array([np.abs(g - r).max() / np.abs(r).max() for g, r in zip(out, ref)])
+            msg += f", logits per-request rel err max {rel.max():.3e} mean {rel.mean():.3e} (revisits max {rel[32:].max():.3e})"
+        print(msg)
         if mode == "hierarchical":
             assert rep["evictions"] > 0 and rep["hist_host"] > 0  # the evict -> onload path ran
         if mode == "hierarchical+adaptive":  # both ways of materialising a host hit ran
             assert rep["prefix_recomputed"] > 0 and rep["prefix_onloaded"] > 0, rep
-        assert rel.max() <= LOGIT_REL
-        got[mode] = out
+        assert kv_err.max() <= KV_REL
+        if check_logits:
+            assert rel.max() <= LOGIT_REL
+        got[mode], got_kv[mode] = out, kv_last
     for a, b in [("hierarchical", "gpu_only"), ("hierarchical", "recompute"), ("gpu_only", "recompute"),
                  ("hierarchical", "hierarchical+adaptive")]:
-        x = max(np.abs(g - h).max() / np.abs(r).max() for g, h, r in zip(got[a], got[b], ref))
-        print(f"mode invariance {a} vs {b}: max rel {x:.3e}")
-        assert x <= MODE_REL
+        msg = f"L={L} mode invariance {a} vs {b}:"
+        if "recompute" not in (a, b):
+            assert got_kv[a].keys() == got_kv[b].keys()
+            xk = max(float(np.abs(ga - gb).max() / np.abs(ga).max()) for key in got_kv[a]
+                     for ga, gb in zip(got_kv[a][key], got_kv[b][key]))
+            msg += f" K/V max rel {xk:.3e}"
+            assert xk <= MODE_REL
+        if check_logits:
+            x = max(np.abs(g - h).max() / np.abs(r).max() for g, h, r in zip(got[a], got[b], ref))
+            msg += f", logits max rel {x:.3e}"
+            assert x <= MODE_REL_LOGIT
+        print(msg)

@@ -71,6 +71,7 @@ def main():
     ap.add_argument("--config", default="gr4_d256")
     ap.add_argument("--users", type=int, default=0)
     ap.add_argument("--trace", default="", help="also write a chrome trace (JSON) here")
+    ap.add_argument("--policy", default="adaptive", choices=["adaptive", "always"], help="host-hit onload policy")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -86,7 +87,7 @@ def main():
     extent_mb = -(-((cfg["history"] + 16 * cfg["delta"]) * tok) // 2**20)
     eng = mtkv.Engine(kv, mtkv.CostModel(bus_bandwidth=55e9), mode="hierarchical", backend="value", batch_size=B,
                       model=model, host_reserve_mb=int(1.1 * cfg["users"] * extent_mb) + 1024,
-                      host_extent_mb=extent_mb)
+                      host_extent_mb=extent_mb, onload_policy=args.policy)
     pb = max(1, 65536 // cfg["history"])
     for i in range(0, len(prefill), pb):
         eng.process_batch(prefill[i:i + pb])
