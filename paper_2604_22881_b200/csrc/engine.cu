@@ -529,6 +529,9 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   const uint32_t n_items = value_ ? (tc ? plan_.n_ctas() : uint32_t(plan_.items.size())) : 0;
   const uint32_t n_pieces = value_ && tc ? uint32_t(plan_.pieces.size()) : 0;
   const uint32_t n_on = uint32_t(w.onloads.size()), n_off = uint32_t(w.offloads.size());
+  uint32_t n_gblk = 0;  // gate/norm row blocks
+  if (value_)
+    for (uint32_t r = 0; r < n; ++r) n_gblk += (rd[r].n_q + kGateBlockRows - 1) / kGateBlockRows;
 
   size_t need = 0;
   need = align16(need + n * sizeof(ReqDev));
@@ -543,6 +546,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   need = align16(need + (tc ? n_items + 1 : 0) * sizeof(uint32_t));
   need = align16(need + (n_on + n_off) * sizeof(ChunkWork));
   need = align16(need + 2 * ncand_total * sizeof(uint32_t));
+  need = align16(need + 2 * n_gblk * sizeof(uint32_t));
   if (meta_host_bytes_[k] < need) {
     if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
     meta_host_bytes_[k] = std::max(need, meta_host_bytes_[k] * 2);
@@ -578,6 +582,13 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   uint32_t* h_creq = carve<uint32_t>(hb, off, ncand_total);
   uint32_t* h_cid = h_creq + ncand_total;
   off = align16(o_cand + 2 * ncand_total * sizeof(uint32_t));
+  const size_t o_gblk = off;
+  uint32_t* h_gblk = carve<uint32_t>(hb, off, 2 * n_gblk);
+  for (uint32_t r = 0, b = 0; r < n && value_; ++r)
+    for (uint32_t i0 = 0; i0 < rd[r].n_q; i0 += kGateBlockRows, ++b) {
+      h_gblk[2 * b] = r;
+      h_gblk[2 * b + 1] = i0;
+    }
 
   std::memcpy(h_req, rd.data(), n * sizeof(ReqDev));
   if (!pages.empty()) std::memcpy(h_pages, pages.data(), pages.size() * sizeof(uint32_t));
@@ -798,6 +809,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       GateArgs gn{};
       gn.part_o = aa.part_o; gn.part_lse = aa.part_lse; gn.segs = d_segs; gn.bm = bq; gn.u = U; gn.ln_scale = w_ln_ + size_t(l) * d;
       gn.row_req = d_rr; gn.reqs = d_req; gn.out = X2; gn.rows = rows; gn.H = H; gn.D = g_.D;
+      gn.blocks = reinterpret_cast<const uint32_t*>(db + o_gblk); gn.n_blocks = n_gblk;
       launch_gate_norm(gn, comp_);
       GemmArgs m1{};
       m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = rows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID; m1.pdl = true;

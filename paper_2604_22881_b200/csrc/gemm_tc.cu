@@ -15,7 +15,10 @@
 #include <cstdio>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <deque>
+#include <string>
 
 #include "kernels.cuh"
 
@@ -228,6 +231,188 @@ __global__ void __launch_bounds__(128)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
+// ------------------------------------------------------------ persistent ---
+// Persistent, warp-specialised form (every shape gemm_tc_supported covers with
+// K <= 256): CTA c owns output column tile nt = c % NT (BN = 128 columns) for
+// the CTA's whole life and walks the M tiles c / NT, c / NT + MC, ... Its W
+// column block [K x 128] is loaded into shared memory once; only A streams
+// (TMA ring of 16 KB k-blocks). Two TMEM accumulators let the MMA warp start
+// tile i+1 while 8 epilogue warps drain tile i (2 per SMSP: warp e reads TMEM
+// lane quadrant e % 4, column half e / 4), apply the fused epilogue and leave
+// through a per-warp swizzled staging tile as 128-B row segments.
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..9 epilogue.
+namespace gps {
+constexpr int BN = 128, EPI_WARPS = 8, THREADS = (2 + EPI_WARPS) * 32;
+constexpr uint32_t A_KB = BM * BK * 2;            // 16 KB per A k-block
+constexpr uint32_t W_KB = BK * BN * 2;            // 16 KB per W k-block
+constexpr uint32_t STAGE_W = 32 * 64 * 2;         // per-warp staging: 32 rows x 64 columns bf16
+// K <= 256 (d = 256 layers): 64 KB of W, 6 A stages; K <= 512 (d = 512): 128 KB of W, 4 A stages
+template <int KMAX, int NA>
+constexpr size_t smem_bytes() { return 1024 + size_t(KMAX / BK) * W_KB + NA * A_KB + EPI_WARPS * STAGE_W + 256; }
+}  // namespace gps
+
+// silu(x) = x * sigmoid(x) = x * (0.5 + 0.5 tanh(x / 2)): one MUFU op (tanh.approx)
+// instead of ex2 + rcp; the result is rounded to bf16 (2^-8) and tanh.approx is
+// good to ~2^-11
+__device__ __forceinline__ float silu_t(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return x * fmaf(0.5f, t, 0.5f);
+}
+
+template <int KMAX, int NA>
+__global__ void __launch_bounds__(gps::THREADS, 1)
+    gemm_ps_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap w_map, GemmArgs g) {
+  using namespace gps;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nk = g.K / BK;
+  uint8_t* sW = smem;                                   // [nk][BN/64][64 k x 128 B]
+  uint8_t* sA = sW + size_t(KMAX / BK) * W_KB;          // [NA] A k-blocks
+  uint8_t* sStage = sA + NA * A_KB;                     // [8 warps][32 rows x 128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + EPI_WARPS * STAGE_W);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + NA;
+  uint64_t* w_full = a_empty + NA;
+  uint64_t* acc_full = w_full + 1;   // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int NT = g.N / BN;
+  const int nt = int(blockIdx.x) % NT, mc = int(gridDim.x) / NT;
+  const int MT = (g.M + BM - 1) / BM;
+  const int n0 = nt * BN;
+  const int my_tiles = int(blockIdx.x) / NT < MT ? (MT - 1 - int(blockIdx.x) / NT) / mc + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NA; ++s) { mbar_init(&a_full[s], 1); mbar_init(&a_empty[s], 1); }
+    mbar_init(w_full, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tslot)), "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // the weights are not written by the predecessor: load them ahead of the PDL wait
+      mbar_expect_tx(w_full, uint32_t(nk) * W_KB);
+      for (int kb = 0; kb < nk; ++kb)
+#pragma unroll
+        for (int b = 0; b < BN / 64; ++b)
+          tma_load_2d(sW + kb * W_KB + b * (BK * 128), &w_map, n0 + 64 * b, kb * BK, w_full);
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // A is the predecessor's output
+      int it = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        const int m0 = (int(blockIdx.x) / NT + t * mc) * BM;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % NA;
+          if (it >= NA) mbar_wait(&a_empty[st], ((it / NA) - 1) & 1);
+          mbar_expect_tx(&a_full[st], A_KB);
+          tma_load_2d(sA + st * A_KB, &a_map, kb * BK, m0, &a_full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc =
+          (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+      mbar_wait(w_full, 0);
+      int it = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        const int b = t & 1;
+        if (t >= 2) mbar_wait(&acc_empty[b], ((t >> 1) - 1) & 1);  // epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + b * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int st = it % NA;
+          mbar_wait(&a_full[st], (it / NA) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = s32(sA + st * A_KB), sw = s32(sW + kb * W_KB);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_ss(d, sdesc(sa + kk * 32, 16, 1024), sdesc(sw + kk * 2048, BK * 128, 1024), idesc,
+                   (kb > 0 || kk > 0) ? 1u : 0u);
+          commit(&a_empty[st]);
+        }
+        commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // ---- epilogue warps ----
+    const uint32_t e = warp - 2, q = warp % 4, ch = e / 4;  // TMEM lane quadrant, column half
+    uint4* stg = reinterpret_cast<uint4*>(sStage + e * STAGE_W);  // [32 rows][8 chunks of 16 B], swizzled
+    const bool act = g.epi != Epi::Bf16;
+    const int col0 = n0 + int(ch) * 64;  // this warp's first output column
+    const uint32_t part = g.epi == Epi::Proj ? uint32_t(col0) / g.d : 0u, w = g.epi == Epi::Proj ? uint32_t(col0) % g.d : 0u;
+    for (int t = 0; t < my_tiles; ++t) {
+      const int b = t & 1;
+      const int m0 = (int(blockIdx.x) / NT + t * mc) * BM;
+      // K / V columns: the pool offsets of this warp's 32 rows, one load per lane
+      // issued ahead of the accumulator wait (the store loop below would
+      // otherwise wait on a dependent load per row)
+      uint64_t kv_lane = 0;
+      if (part >= 2 && m0 + int(q) * 32 + int(lane) < g.M) kv_lane = g.kv_off[m0 + int(q) * 32 + int(lane)];
+      mbar_wait(&acc_full[b], (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + ((32u * q) << 16) + b * BN + ch * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(taddr + c * 32, v);
+        if (c == 1) {  // both halves of this warp's 64 columns are in registers: release the accumulator
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(&acc_empty[b])) : "memory");
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float x[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = act ? silu_t(v[8 * i + j]) : v[8 * i + j];
+          uint4 pk;
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]), h1 = __floats2bfloat162_rn(x[2], x[3]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(x[4], x[5]), h3 = __floats2bfloat162_rn(x[6], x[7]);
+          pk.x = *reinterpret_cast<uint32_t*>(&h0);
+          pk.y = *reinterpret_cast<uint32_t*>(&h1);
+          pk.z = *reinterpret_cast<uint32_t*>(&h2);
+          pk.w = *reinterpret_cast<uint32_t*>(&h3);
+          stg[lane * 8 + ((c * 4 + i) ^ (lane & 7))] = pk;
+        }
+      }
+      __syncwarp();
+      // 32 rows x 128 B: 8 lanes per row, 4 rows per store instruction
+      const int ck = int(lane) % 8;
+#pragma unroll
+      for (int rr = int(lane) / 8; rr < 32; rr += 4) {
+        const int row = m0 + int(q) * 32 + rr;
+        const uint64_t kvo = __shfl_sync(0xffffffffu, kv_lane, rr);  // every lane: no early exit before it
+        if (row >= g.M) continue;
+        const uint4 val = stg[rr * 8 + (ck ^ (rr & 7))];
+        __nv_bfloat16* dst;
+        if (g.epi == Epi::Proj)
+          dst = part == 0   ? g.out_u + size_t(row) * g.d + w + ck * 8
+                : part == 1 ? g.out_q + size_t(row) * g.d + w + ck * 8
+                            : g.pool + g.layer_base + kvo + (part == 3 ? g.kv_stride : 0) + w + ck * 8;
+        else
+          dst = static_cast<__nv_bfloat16*>(g.out) + size_t(row) * g.N + col0 + ck * 8;
+        *reinterpret_cast<uint4*>(dst) = val;
+      }
+      __syncwarp();  // the staging tile is rewritten by the next tile
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * gps::BN));
+}
+
 // ------------------------------------------------------------------ host ---
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_g() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -305,14 +490,51 @@ static bool cached_map(CUtensorMap* out, const void* base, uint64_t cols, uint64
   return true;
 }
 
+// MTKV_GEMM=tile: the one-CTA-per-tile kernel everywhere (A/B switch)
+static bool gemm_ps_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MTKV_GEMM");
+    return !(e && std::string(e) == "tile");
+  }();
+  return on;
+}
+
 // A: [M x K] activations (rows padded by TMA zero fill), W: [K x N] row-major weights
 int launch_gemm_tc(const GemmArgs& a, uint64_t a_rows_alloc, cudaStream_t s) {
   if (a.M <= 0) return 0;
   alignas(64) CUtensorMap am, wm;
   if (!cached_map(&am, a.A, a.K, a_rows_alloc, BK, BM) || !cached_map(&wm, a.B, a.N, a.K, 64, BK)) return -1;
-  // wide N (projection, 4d): 128-column tiles (measured 16.5 us vs 18.7 us with
-  // 64-column tiles, and a 415 vs 439 us layer-stack span against 256-column
-  // tiles at 2 CTAs per SM); narrow N (MLP, d): 64-column tiles
+  if (gemm_ps_enabled() && a.N % gps::BN == 0 && a.K <= 512 && (a.epi != Epi::Proj || a.d % 64 == 0)) {
+    const int NT = a.N / gps::BN, MT = (a.M + BM - 1) / BM;
+    const int mc = std::max(1, std::min(num_sms() / NT, MT));  // CTAs per column tile
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(NT * mc);
+    cfg.blockDim = dim3(gps::THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+    if (a.K <= 256) {
+      constexpr size_t sm = gps::smem_bytes<256, 6>();
+      static DeviceOnce once;
+      if (once.first()) cudaFuncSetAttribute(gemm_ps_kernel<256, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+      cfg.dynamicSmemBytes = sm;
+      cudaLaunchKernelEx(&cfg, gemm_ps_kernel<256, 6>, am, wm, a);
+    } else {
+      constexpr size_t sm = gps::smem_bytes<512, 4>();
+      static_assert(sm <= 232448, "shared memory budget");
+      static DeviceOnce once;
+      if (once.first()) cudaFuncSetAttribute(gemm_ps_kernel<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+      cfg.dynamicSmemBytes = sm;
+      cudaLaunchKernelEx(&cfg, gemm_ps_kernel<512, 4>, am, wm, a);
+    }
+    return 0;
+  }
+  // one CTA per tile. Wide N (projection, 4d): 128-column tiles (measured 16.5 us
+  // vs 18.7 us with 64-column tiles, and a 415 vs 439 us layer-stack span against
+  // 256-column tiles at 2 CTAs per SM); narrow N (MLP, d): 64-column tiles
   if (a.N >= 1024) launch_bn<128>(am, wm, a, s);
   else launch_bn<64>(am, wm, a, s);
   return 0;

@@ -195,16 +195,23 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s) {
   else gemm_kernel<false><<<grid, 128, 0, s>>>(a);
 }
 
+// one warp per row: 16-B vector copies of the token's embedding row when d % 8 == 0
 __global__ void embed_kernel(__nv_bfloat16* x, const __nv_bfloat16* table, const uint32_t* tok, int rows, int d) {
-  const int r = blockIdx.x;
+  const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (r >= rows) return;
   const __nv_bfloat16* src = table + (size_t)tok[r] * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) x[(size_t)r * d + j] = src[j];
+  __nv_bfloat16* dst = x + (size_t)r * d;
+  if (d % 8 == 0) {
+    for (int j = lane * 8; j < d; j += 32 * 8)
+      *reinterpret_cast<uint4*>(dst + j) = *reinterpret_cast<const uint4*>(src + j);
+  } else {
+    for (int j = lane; j < d; j += 32) dst[j] = src[j];
+  }
 }
 
 void launch_embed(__nv_bfloat16* x, const __nv_bfloat16* table, const uint32_t* tok, int rows, int d,
                   cudaStream_t s) {
-  if (rows > 0) embed_kernel<<<rows, 128, 0, s>>>(x, table, tok, rows, d);
+  if (rows > 0) embed_kernel<<<(rows + 7) / 8, 256, 0, s>>>(x, table, tok, rows, d);
 }
 
 // -------------------------------------------------------------- attention ---
@@ -596,9 +603,128 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
   }
 }
 
+// Row-block form (the common shapes: d % 32 == 0, H in {1, 2, 4, 8}, D % 4 == 0):
+// one CTA per 32 query rows of one request's query tile. Warp w owns the d/8
+// columns [w d/8, (w+1) d/8) (one head), lane = row, so every partial-slot
+// read is one 4-column chunk of 32 consecutive rows = 512 contiguous bytes
+// (the chunked slot layout, part_index); the gate operand u is staged through
+// shared memory with row-contiguous loads, the row statistics are reduced
+// across the 8 warps in shared memory, and the normalised rows leave through
+// shared memory as row-contiguous 16-B stores. The request / segment / slot
+// metadata is loaded once per block instead of once per row.
+constexpr int GB_WARPS = 8;
+bool gate_block_supported(uint32_t H, uint32_t D) {
+  const uint32_t d = H * D;
+  return d % 32 == 0 && d <= 512 && D % 4 == 0 && (H == 1 || H == 2 || H == 4 || H == 8);
+}
+
+template <int CPW>  // 4-column chunks per warp (d / 32)
+__global__ void __launch_bounds__(GB_WARPS * 32) gate_block_kernel(GateArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int NC = CPW * 4;                      // columns per warp
+  constexpr int d = NC * GB_WARPS;
+  constexpr int UP = d + 8;                        // padded bf16 row stride in shared memory
+  __shared__ __align__(16) __nv_bfloat16 s_u[kGateBlockRows * UP];  // u rows, later the output rows
+  __shared__ float s_red[GB_WARPS][kGateBlockRows];
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t req = a.blocks[2 * blockIdx.x], i0 = a.blocks[2 * blockIdx.x + 1];
+  const ReqDev R = a.reqs[req];
+  const uint32_t nrows = min(kGateBlockRows, R.n_q - i0);
+  const size_t row0 = size_t(R.q_row0) + i0;       // global row of block row 0
+  // stage u (row-contiguous 16-B loads)
+  constexpr int V16 = d / 8;                       // 16-B vectors per row
+  for (uint32_t v = threadIdx.x; v < kGateBlockRows * V16; v += GB_WARPS * 32) {
+    const uint32_t rr = v / V16, cv = v % V16;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (rr < nrows) x = *reinterpret_cast<const uint4*>(a.u + (row0 + rr) * d + cv * 8);
+    *reinterpret_cast<uint4*>(s_u + rr * UP + cv * 8) = x;
+  }
+  // merge this warp's head's partial slots for row `lane`
+  const uint32_t c0 = warp * NC, h = c0 / a.D, cd = c0 % a.D;   // first column, head, column within the head
+  const uint32_t qt = i0 / a.bm, ri = i0 % a.bm + lane;
+  const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
+  const bool valid = lane < nrows;
+  float mx = -INFINITY;
+  for (uint32_t k = 0; k < sg.n_parts; ++k) mx = fmaxf(mx, a.part_lse[size_t(sg.part_base + k) * a.bm + ri]);
+  float acc[NC];
+#pragma unroll
+  for (int e = 0; e < NC; ++e) acc[e] = 0.f;
+  float den = 0.f;
+  for (uint32_t k = 0; k < sg.n_parts; ++k) {
+    const float l = a.part_lse[size_t(sg.part_base + k) * a.bm + ri];
+    if (!valid || l == -INFINITY) continue;
+    const float w = exp2f(l - mx);
+    den += w;
+    const float* src = a.part_o + part_index(sg.part_base + k, a.bm, ri, cd, a.D);
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      const float4 v = *reinterpret_cast<const float4*>(src + size_t(c) * a.bm * 4);
+      acc[4 * c] += w * v.x; acc[4 * c + 1] += w * v.y; acc[4 * c + 2] += w * v.z; acc[4 * c + 3] += w * v.w;
+    }
+  }
+  __syncthreads();  // u staged
+  const float inv_den = den > 0.f ? 1.f / den : 0.f;
+  float sum = 0.f;
+#pragma unroll
+  for (int e = 0; e < NC; e += 2) {
+    const float2 u2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(s_u + lane * UP + c0 + e));
+    acc[e] = silu_f(acc[e] * inv_den) * u2.x;
+    acc[e + 1] = silu_f(acc[e + 1] * inv_den) * u2.y;
+    sum += acc[e] + acc[e + 1];
+  }
+  s_red[warp][lane] = sum;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < GB_WARPS; ++w) tot += s_red[w][lane];
+  const float mean = tot / float(d);
+  float var = 0.f;
+#pragma unroll
+  for (int e = 0; e < NC; ++e) { const float c = acc[e] - mean; var += c * c; }
+  __syncthreads();  // everyone read the sums
+  s_red[warp][lane] = var;
+  __syncthreads();
+  float vt = 0.f;
+#pragma unroll
+  for (int w = 0; w < GB_WARPS; ++w) vt += s_red[w][lane];
+  const float rstd = 1.0f / sqrtf(vt / float(d) + 1e-6f);
+  // normalised row -> shared memory (over u, which every thread has read), then out
+#pragma unroll
+  for (int e = 0; e < NC; e += 2) {
+    const float2 sc = *reinterpret_cast<const float2*>(a.ln_scale + c0 + e);
+    *reinterpret_cast<__nv_bfloat162*>(s_u + lane * UP + c0 + e) =
+        __floats2bfloat162_rn((acc[e] - mean) * rstd * sc.x, (acc[e + 1] - mean) * rstd * sc.y);
+  }
+  __syncthreads();
+  for (uint32_t v = threadIdx.x; v < kGateBlockRows * V16; v += GB_WARPS * 32) {
+    const uint32_t rr = v / V16, cv = v % V16;
+    if (rr < nrows) *reinterpret_cast<uint4*>(a.out + (row0 + rr) * d + cv * 8) = *reinterpret_cast<const uint4*>(s_u + rr * UP + cv * 8);
+  }
+}
+
 void launch_gate_norm(const GateArgs& a, cudaStream_t s) {
   if (a.rows == 0) return;
   const uint32_t d = a.H * a.D, E = d % 32 == 0 ? d / 32 : 0;
+  if (a.blocks && a.n_blocks && gate_block_supported(a.H, a.D)) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.n_blocks);
+    cfg.blockDim = dim3(GB_WARPS * 32);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    switch (d / 32) {
+      case 1: cudaLaunchKernelEx(&cfg, gate_block_kernel<1>, a); return;
+      case 2: cudaLaunchKernelEx(&cfg, gate_block_kernel<2>, a); return;
+      case 4: cudaLaunchKernelEx(&cfg, gate_block_kernel<4>, a); return;
+      case 8: cudaLaunchKernelEx(&cfg, gate_block_kernel<8>, a); return;
+      case 16: cudaLaunchKernelEx(&cfg, gate_block_kernel<16>, a); return;
+      default: break;  // other widths: the row-per-warp kernel below
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.rows + GATE_WARPS - 1) / GATE_WARPS);
   cfg.blockDim = dim3(GATE_WARPS * 32);

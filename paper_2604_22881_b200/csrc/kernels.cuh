@@ -144,7 +144,13 @@ struct GateArgs {  // split combine + silu(o) * u + layer norm -> bf16 (launched
   const ReqDev* reqs;
   __nv_bfloat16* out;
   uint32_t rows, H, D;
+  // row blocks (gate_block_kernel): (request, first query index) pairs, 32
+  // query rows of one request each, aligned to the bm-row query tiles
+  const uint32_t* blocks = nullptr;
+  uint32_t n_blocks = 0;
 };
+constexpr uint32_t kGateBlockRows = 32;
+bool gate_block_supported(uint32_t H, uint32_t D);
 void launch_gate_norm(const GateArgs& a, cudaStream_t s);
 
 void launch_scatter_chunks(__nv_bfloat16* pool, const __nv_bfloat16* staging, const ChunkWork* work,

@@ -71,6 +71,8 @@ def main():
     ap.add_argument("--config", default="gr4_d256")
     ap.add_argument("--users", type=int, default=0)
     ap.add_argument("--trace", default="", help="also write a chrome trace (JSON) here")
+    ap.add_argument("--ncu", action="store_true", help="bracket the measured batches with cudaProfilerStart/Stop "
+                    "(run under ncu --profile-from-start off) instead of torch.profiler")
     ap.add_argument("--policy", default="adaptive", choices=["adaptive", "always"], help="host-hit onload policy")
     args = ap.parse_args()
     import torch
@@ -96,6 +98,14 @@ def main():
         eng.process_batch(None, packed=batches[i])
     eng.synchronize()
     torch.cuda.synchronize()
+    if args.ncu:  # ncu --profile-from-start off: only the measured batches are captured
+        torch.cuda.profiler.start()
+        for i in range(args.warm, args.warm + args.steps):
+            eng.process_batch(None, packed=batches[i])
+        eng.synchronize()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for i in range(args.warm, args.warm + args.steps):
             eng.process_batch(None, packed=batches[i])
