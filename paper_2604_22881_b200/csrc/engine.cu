@@ -179,13 +179,12 @@ int Engine::init(std::string& err) {
     err = "engine: the device pool stores bf16 (bytes_per_element must be 2)";
     return MTKV_ERROR;
   }
-  // tcgen05 attention for every production shape; the mma.sync kernel covers
-  // head_dim < 64 (the reference's tiny test models). MTKV_ATTN=mma forces it
-  // for A/B measurements.
-  {
-    const char* f = std::getenv("MTKV_ATTN");
-    use_tc_ = attn_tc_supported(g_) && !(f && std::string(f) == "mma");
-  }
+  // tcgen05 attention for every production shape: the two-lane kernel for
+  // head_dim 64/128, the column-split one for head_dim 32; the mma.sync kernel
+  // covers the reference's tiny test models (attn_kind: MTKV_ATTN=mma|tc1 force
+  // the others for A/B measurements)
+  attn_kind_ = attn_kind(g_);
+  use_tc_ = attn_kind_ != AttnKind::Mma;
   n_sm_ = num_sms();
   CK(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
@@ -523,7 +522,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     max_hist = std::max(max_hist, x.n_hist);
   }
   last_rows_ = rows;
-  if (value_) plan_attention(rd.data(), n, g_, tc, tc ? uint32_t(n_sm_) : 0, plan_);
+  if (value_) {
+    plan_attention(rd.data(), n, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_);
+    if (attn_kind_ == AttnKind::Pp && plan_.n_ctas() % 2) plan_.cta_off.push_back(plan_.cta_off.back());
+  }
   const uint32_t bq = plan_.bm;
   const uint32_t n_segs = value_ ? uint32_t(plan_.segs.size()) : 0;
   const uint32_t n_items = value_ ? (tc ? plan_.n_ctas() : uint32_t(plan_.items.size())) : 0;
@@ -800,10 +802,8 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
           q_map_ptr_ = q_.p;
           q_map_bytes_ = q_.bytes;
         }
-        launch_attention_tc(pool_map_, q_map_, aa, comp_);
-      } else {
-        launch_attention(aa, comp_);
       }
+      launch_attention_any(attn_kind_, pool_map_, q_map_, aa, comp_);
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l + 1], comp_));
       ++attn_launches_last_;
       GateArgs gn{};

@@ -117,7 +117,8 @@ class Engine {
   __nv_bfloat16 *w_embed_ = nullptr, *w_in_ = nullptr, *w1_ = nullptr, *w2_ = nullptr, *w_out_ = nullptr;
   float* w_ln_ = nullptr;
   uint32_t staging_slots_ = 0;
-  bool use_tc_ = false;          // tcgen05 attention (head_dim 64/128)
+  bool use_tc_ = false;          // a tcgen05 attention kernel (attn_kind_ != Mma)
+  AttnKind attn_kind_ = AttnKind::Mma;
   int n_sm_ = 1;                 // persistent attention CTAs
   DevCtl ctl_;                   // device control plane (opt_.device_planner)
   double last_plan_ms_ = 0;

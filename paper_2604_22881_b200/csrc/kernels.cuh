@@ -183,6 +183,18 @@ int make_pool_map(CUtensorMap* map, const void* pool, const PoolGeom& g);
 int make_q_map(CUtensorMap* map, const void* q, uint64_t rows, const PoolGeom& g);
 void launch_attention_tc(const CUtensorMap& pool_map, const CUtensorMap& q_map,
                          const AttnArgs& a, cudaStream_t s);
+// two-lane form (attn_pp.cu): head_dim 64/128; planned over 2 x SMs virtual CTAs
+// (an even count: CTA b runs virtual CTAs 2b and 2b + 1)
+bool attn_pp_supported(const PoolGeom& g);
+void launch_attention_pp(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a, cudaStream_t s);
+// which attention kernel serves geometry g (attn_pp.cu: MTKV_ATTN=pp|mma select
+// the two-lane or the mma.sync kernel for A/B measurements), and the virtual
+// CTAs to plan for
+enum class AttnKind { Mma, Tc, Pp };
+AttnKind attn_kind(const PoolGeom& g);
+uint32_t attn_plan_ctas(AttnKind k, int n_sm);
+void launch_attention_any(AttnKind k, const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a,
+                          cudaStream_t s);
 int num_sms();
 
 // once per CUDA device (kernel attributes such as the dynamic smem opt-in are

@@ -110,10 +110,11 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
   std::vector<uint32_t> row_req(rows);
   for (uint32_t r = 0; r < n_req; ++r)
     for (uint32_t i = 0; i < n_q[r]; ++i) row_req[rq[r].q_row0 + i] = r;
-  const char* force = std::getenv("MTKV_ATTN");
-  const bool tc = attn_tc_supported(g) && !(force && std::string(force) == "mma");
+  const AttnKind kind = attn_kind(g);
+  const bool tc = kind != AttnKind::Mma;
   AttnPlan plan;
-  plan_attention(rq.data(), n_req, g, tc, tc ? uint32_t(num_sms()) : 0, plan);
+  plan_attention(rq.data(), n_req, g, tc, attn_plan_ctas(kind, num_sms()), plan);
+  if (kind == AttnKind::Pp && plan.n_ctas() % 2) plan.cta_off.push_back(plan.cta_off.back());
   const uint32_t n_items = tc ? plan.n_ctas() : uint32_t(plan.items.size());
   // one device allocation: requests | rows | segments | items or pieces + CTA offsets | lse | partials
   size_t off = 0;
@@ -185,8 +186,7 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
         cudaMemsetAsync(flush, int(it & 0xFF), size_t(256) << 20, s);
         cudaEventRecord(ev[2 * (it - 1)], s);
       }
-      if (tc) launch_attention_tc(pmap, qmap, a, s);
-      else launch_attention(a, s);
+      launch_attention_any(kind, pmap, qmap, a, s);
       if (it >= 1 && !ev.empty()) cudaEventRecord(ev[2 * (it - 1) + 1], s);
     }
     if (!ev.empty()) {

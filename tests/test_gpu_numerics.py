@@ -240,3 +240,18 @@ def test_value_engine_configs1_dims_evict_onload_all_modes_vs_fp64(L):
             msg += f", logits max rel {x:.3e}"
             assert x <= MODE_REL_LOGIT
         print(msg)
+
+
+def test_two_lane_attention_kernel_same_bars():
+    """The two-lane attention kernel (attn_pp.cu, MTKV_ATTN=pp; an A/B variant,
+    not the default) against the same peaked / poisoned bars: the kernel choice
+    is fixed per process, so the shapes run in a child process."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_numerics.py"), "-q", "-x",
+                        "-p", "no:cacheprovider", "-k", "relative_bar and not -32-"],
+                       env={**os.environ, "MTKV_ATTN": "pp"}, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-400:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
