@@ -59,6 +59,32 @@ void DevBuf::release() {
   bytes = 0;
 }
 
+// Candidate scores without the full-vocabulary head (rank_candidates only reads
+// the candidates' logits, model.cpp:199): one warp per candidate, the dot of the
+// request's last hidden row with the candidate's row of w_out^T (16-B loads).
+__global__ void candidate_scores_kernel(float* out, const __nv_bfloat16* x, const __nv_bfloat16* w_out_t,
+                                        const uint32_t* last_row, const uint32_t* creq, const uint32_t* cid,
+                                        uint32_t n, uint32_t d) {
+  const uint32_t j = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (j >= n) return;
+  const __nv_bfloat16* xr = x + size_t(last_row[creq[j]]) * d;
+  const __nv_bfloat16* wr = w_out_t + size_t(cid[j]) * d;
+  float acc = 0.f;
+  for (uint32_t k = lane * 8; k < d; k += 256) {
+    const uint4 a = *reinterpret_cast<const uint4*>(xr + k), b = *reinterpret_cast<const uint4*>(wr + k);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
+      acc = fmaf(fa.x, fb.x, fmaf(fa.y, fb.y, acc));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[j] = acc;
+}
+
 __global__ void pick_scores_kernel(float* out, const float* logits, const uint32_t* creq,
                                    const uint32_t* cid, uint32_t n, uint32_t vocab) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -93,7 +119,7 @@ Engine::~Engine() {
   DevBuf* bufs[] = {&trace_, &pool_, &staging_[0], &staging_[1], &offload_, &meta_, &x_, &x2_, &u_, &q_,
                     &mid_, &part_o_, &part_lse_, &logits_, &scores_};
   for (DevBuf* b : bufs) b->release();
-  for (void* p : {(void*)w_embed_, (void*)w_in_, (void*)w1_, (void*)w2_, (void*)w_out_, (void*)w_ln_})
+  for (void* p : {(void*)w_embed_, (void*)w_in_, (void*)w1_, (void*)w2_, (void*)w_out_, (void*)w_out_t_, (void*)w_ln_})
     if (p) cudaFree(p);
   for (char* s : slabs_) cudaFreeHost(s);
   for (int k = 0; k < kRing; ++k) {
@@ -153,6 +179,13 @@ void Engine::init_weights() {
   up(w1, &w1_);
   up(w2, &w2_);
   up(w_out, &w_out_);
+  // w_out^T [V x d] for the candidate-score kernel (one contiguous row per candidate)
+  if (d % 8 == 0) {
+    std::vector<__nv_bfloat16> wt(V * d);
+    for (size_t k = 0; k < d; ++k)
+      for (size_t v = 0; v < V; ++v) wt[v * d + k] = w_out[k * V + v];
+    up(wt, &w_out_t_);
+  }
   up(ln, &w_ln_);
 }
 
@@ -819,13 +852,21 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       if (gemm(m2, mid_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       launches += 5;
     }
-    GemmArgs hd{};
-    hd.A = X; hd.row_idx = d_last; hd.B = w_out_; hd.M = n; hd.N = V; hd.K = d; hd.epi = Epi::F32; hd.out = logits_.p;
-    launch_gemm(hd, comp_);
-    ++launches;
-    if (ncand_total) {
-      pick_scores_kernel<<<(ncand_total + 127) / 128, 128, 0, comp_>>>(
-          static_cast<float*>(scores_.p), static_cast<const float*>(logits_.p), d_creq, d_cid, ncand_total, V);
+    if (opt_.keep_logits || !w_out_t_) {
+      // full-vocabulary logits (kept for the caller), candidates picked from them
+      GemmArgs hd{};
+      hd.A = X; hd.row_idx = d_last; hd.B = w_out_; hd.M = n; hd.N = V; hd.K = d; hd.epi = Epi::F32; hd.out = logits_.p;
+      launch_gemm(hd, comp_);
+      ++launches;
+      if (ncand_total) {
+        pick_scores_kernel<<<(ncand_total + 127) / 128, 128, 0, comp_>>>(
+            static_cast<float*>(scores_.p), static_cast<const float*>(logits_.p), d_creq, d_cid, ncand_total, V);
+        ++launches;
+      }
+    } else if (ncand_total) {
+      // serving: only the candidates' scores are ever read
+      candidate_scores_kernel<<<(ncand_total + 7) / 8, 256, 0, comp_>>>(static_cast<float*>(scores_.p), X, w_out_t_,
+                                                                      d_last, d_creq, d_cid, ncand_total, d);
       ++launches;
     }
     if (calibrate_) CK(cudaEventRecord(ev_stk1_[k], comp_));

@@ -115,6 +115,7 @@ class Engine {
   // device memory
   DevBuf pool_, staging_[2], offload_, meta_, x_, x2_, u_, q_, mid_, part_o_, part_lse_, logits_, scores_;
   __nv_bfloat16 *w_embed_ = nullptr, *w_in_ = nullptr, *w1_ = nullptr, *w2_ = nullptr, *w_out_ = nullptr;
+  __nv_bfloat16* w_out_t_ = nullptr;  // w_out transposed [V x d] (candidate scores)
   float* w_ln_ = nullptr;
   uint32_t staging_slots_ = 0;
   bool use_tc_ = false;          // a tcgen05 attention kernel (attn_kind_ != Mma)

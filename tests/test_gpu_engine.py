@@ -215,6 +215,34 @@ def test_pipelined_rankings_match_synchronous():
         pipe.rankings(mtkv.Ticket(0, [1, 1]))
 
 
+def test_candidate_scores_match_full_head():
+    """Serving engines (keep_logits off) score only the candidates (one dot product
+    each against w_out^T); engines that keep the logits run the full-vocabulary
+    head and pick. Same inputs: scores agree to fp32 summation order, rankings
+    agree wherever the candidates' logits differ by more than that."""
+    kv = dict(num_layers=2, num_heads=2, head_dim=128, page_size=32, chunk_size=64, device_pages=256,
+              offload_quota=512)
+    mc = mtkv.ModelConfig(num_layers=2, num_heads=2, head_dim=128, vocab=512, seed=5)
+    rng = np.random.default_rng(1)
+    trace = [{"ts": t, "user": t % 5, "dn": 40, "nc": 8, "tokens": rng.integers(0, 512, 40).tolist(),
+              "cands": rng.integers(0, 512, 8).tolist()} for t in range(30)]
+    full = mtkv.Engine(_kv(kv), mode="hierarchical", backend="value", batch_size=3, model=mc, keep_logits=True)
+    serve = mtkv.Engine(_kv(kv), mode="hierarchical", backend="value", batch_size=3, model=mc)
+    checked = 0
+    for b in batches(trace, 3):
+        full.process_batch(b)
+        serve.process_batch(b)
+        lg = full.last_logits()
+        for r, want, got in zip(b, full.last_rankings(), serve.last_rankings()):
+            row = lg[b.index(r)]
+            vals = sorted(set(float(row[c]) for c in r["cands"]))
+            gap = min((y - x for x, y in zip(vals, vals[1:])), default=1.0)
+            if gap > 1e-4 * max(abs(v) for v in vals):
+                assert got == want
+                checked += 1
+    assert checked > 0
+
+
 def test_model_dims_of_bench_config():
     """d = 256 (H=2, D=128): vector/tensor-core paths at the bench width vs the oracle."""
     kv = dict(num_layers=2, num_heads=2, head_dim=128, page_size=32, chunk_size=64, device_pages=64,
