@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(128)
   constexpr uint32_t STG = A_BYTES + W_BYTES;
   constexpr uint32_t TCOLS = BN < 32 ? 32 : BN;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base as an offset into the __shared__ array (keeps the
+  // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTG * STG);
   uint64_t* empty = full + NSTG;
   uint64_t* done = empty + NSTG;
@@ -237,15 +239,18 @@ __global__ void __launch_bounds__(128)
 // the CTA's whole life and walks the M tiles c / NT, c / NT + MC, ... Its W
 // column block [K x 128] is loaded into shared memory once; only A streams
 // (TMA ring of 16 KB k-blocks). Two TMEM accumulators let the MMA warp start
-// tile i+1 while 8 epilogue warps drain tile i (2 per SMSP: warp e reads TMEM
-// lane quadrant e % 4, column half e / 4), apply the fused epilogue and leave
-// through a per-warp swizzled staging tile as 128-B row segments.
-// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..9 epilogue.
+// tile i+1 while 16 epilogue warps drain tile i (4 per SMSP: warp e reads TMEM
+// lane quadrant e % 4, column quarter e / 4), apply the fused epilogue and leave
+// through a per-warp swizzled staging tile as 64-B row segments (the epilogue
+// is latency-bound: 8 warps of 64 columns took 118.5 us for the adaptive
+// batch's projection).
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..17 epilogue.
 namespace gps {
-constexpr int BN = 128, EPI_WARPS = 8, THREADS = (2 + EPI_WARPS) * 32;
+constexpr int BN = 128, EPI_WARPS = 16, THREADS = (2 + EPI_WARPS) * 32;
+constexpr int CW = BN / (EPI_WARPS / 4);          // columns per epilogue warp (32)
 constexpr uint32_t A_KB = BM * BK * 2;            // 16 KB per A k-block
 constexpr uint32_t W_KB = BK * BN * 2;            // 16 KB per W k-block
-constexpr uint32_t STAGE_W = 32 * 64 * 2;         // per-warp staging: 32 rows x 64 columns bf16
+constexpr uint32_t STAGE_W = 32 * CW * 2;         // per-warp staging: 32 rows x CW columns bf16
 // K <= 256 (d = 256 layers): 64 KB of W, 6 A stages; K <= 512 (d = 512): 128 KB of W, 4 A stages
 template <int KMAX, int NA>
 constexpr size_t smem_bytes() { return 1024 + size_t(KMAX / BK) * W_KB + NA * A_KB + EPI_WARPS * STAGE_W + 256; }
@@ -265,7 +270,9 @@ __global__ void __launch_bounds__(gps::THREADS, 1)
     gemm_ps_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap w_map, GemmArgs g) {
   using namespace gps;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base as an offset into the __shared__ array (keeps the
+  // shared address space visible to the compiler: LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (s32(smem_raw) & 1023u)) & 1023u);
   const int nk = g.K / BK;
   uint8_t* sW = smem;                                   // [nk][BN/64][64 k x 128 B]
   uint8_t* sA = sW + size_t(KMAX / BK) * W_KB;          // [NA] A k-blocks
@@ -347,27 +354,32 @@ __global__ void __launch_bounds__(gps::THREADS, 1)
     }
   } else {
     // ---- epilogue warps ----
-    const uint32_t e = warp - 2, q = warp % 4, ch = e / 4;  // TMEM lane quadrant, column half
-    uint4* stg = reinterpret_cast<uint4*>(sStage + e * STAGE_W);  // [32 rows][8 chunks of 16 B], swizzled
+    constexpr int CPR = CW / 8;  // 16-B chunks per staged row
+    const uint32_t e = warp - 2, q = warp % 4, ch = e / 4;  // TMEM lane quadrant, column block
+    uint4* stg = reinterpret_cast<uint4*>(sStage + e * STAGE_W);  // [32 rows][CPR chunks of 16 B], swizzled
     const bool act = g.epi != Epi::Bf16;
-    const int col0 = n0 + int(ch) * 64;  // this warp's first output column
+    const int col0 = n0 + int(ch) * CW;  // this warp's first output column
     const uint32_t part = g.epi == Epi::Proj ? uint32_t(col0) / g.d : 0u, w = g.epi == Epi::Proj ? uint32_t(col0) % g.d : 0u;
+    // K / V columns: the pool offsets of this warp's 32 rows, one load per lane,
+    // fetched one tile ahead (the store loop would otherwise wait on it)
+    auto kv_of = [&](int t) -> uint64_t {
+      const int row = (int(blockIdx.x) / NT + t * mc) * BM + int(q) * 32 + int(lane);
+      return (part >= 2 && t < my_tiles && row < g.M) ? g.kv_off[row] : 0;
+    };
+    uint64_t kv_next = kv_of(0);
     for (int t = 0; t < my_tiles; ++t) {
       const int b = t & 1;
       const int m0 = (int(blockIdx.x) / NT + t * mc) * BM;
-      // K / V columns: the pool offsets of this warp's 32 rows, one load per lane
-      // issued ahead of the accumulator wait (the store loop below would
-      // otherwise wait on a dependent load per row)
-      uint64_t kv_lane = 0;
-      if (part >= 2 && m0 + int(q) * 32 + int(lane) < g.M) kv_lane = g.kv_off[m0 + int(q) * 32 + int(lane)];
+      const uint64_t kv_lane = kv_next;
+      kv_next = kv_of(t + 1);
       mbar_wait(&acc_full[b], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t taddr = tmem + ((32u * q) << 16) + b * BN + ch * 64;
+      const uint32_t taddr = tmem + ((32u * q) << 16) + b * BN + ch * CW;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < CW / 32; ++c) {
         float v[32];
         tmem_ld32(taddr + c * 32, v);
-        if (c == 1) {  // both halves of this warp's 64 columns are in registers: release the accumulator
+        if (c == CW / 32 - 1) {  // this warp's columns are in registers: release the accumulator
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(&acc_empty[b])) : "memory");
@@ -384,18 +396,18 @@ __global__ void __launch_bounds__(gps::THREADS, 1)
           pk.y = *reinterpret_cast<uint32_t*>(&h1);
           pk.z = *reinterpret_cast<uint32_t*>(&h2);
           pk.w = *reinterpret_cast<uint32_t*>(&h3);
-          stg[lane * 8 + ((c * 4 + i) ^ (lane & 7))] = pk;
+          stg[lane * CPR + ((c * 4 + i) ^ ((lane >> 1) & (CPR - 1)))] = pk;
         }
       }
       __syncwarp();
-      // 32 rows x 128 B: 8 lanes per row, 4 rows per store instruction
-      const int ck = int(lane) % 8;
+      // 32 rows x CW*2 B: CPR lanes per row, 32 / CPR rows per store instruction
+      const int ck = int(lane) % CPR;
 #pragma unroll
-      for (int rr = int(lane) / 8; rr < 32; rr += 4) {
+      for (int rr = int(lane) / CPR; rr < 32; rr += 32 / CPR) {
         const int row = m0 + int(q) * 32 + rr;
         const uint64_t kvo = __shfl_sync(0xffffffffu, kv_lane, rr);  // every lane: no early exit before it
         if (row >= g.M) continue;
-        const uint4 val = stg[rr * 8 + (ck ^ (rr & 7))];
+        const uint4 val = stg[rr * CPR + (ck ^ ((rr >> 1) & (CPR - 1)))];
         __nv_bfloat16* dst;
         if (g.epi == Epi::Proj)
           dst = part == 0   ? g.out_u + size_t(row) * g.d + w + ck * 8

@@ -13,6 +13,7 @@
 #include "kernels.cuh"
 
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 namespace mtkv_b200 {
@@ -619,7 +620,7 @@ bool gate_block_supported(uint32_t H, uint32_t D) {
 }
 
 template <int CPW>  // 4-column chunks per warp (d / 32)
-__global__ void __launch_bounds__(GB_WARPS * 32) gate_block_kernel(GateArgs a) {
+__global__ void __launch_bounds__(GB_WARPS * 32, 4) gate_block_kernel(GateArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int NC = CPW * 4;                      // columns per warp
@@ -645,22 +646,33 @@ __global__ void __launch_bounds__(GB_WARPS * 32) gate_block_kernel(GateArgs a) {
   const uint32_t qt = i0 / a.bm, ri = i0 % a.bm + lane;
   const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
   const bool valid = lane < nrows;
+  // the slots' log-sum-exps (up to 4 held in registers: one batch of independent
+  // loads; longer segments reload them), then every slot's chunks issued
+  // without a dependence on the previous slot's
+  float lk[4];
   float mx = -INFINITY;
-  for (uint32_t k = 0; k < sg.n_parts; ++k) mx = fmaxf(mx, a.part_lse[size_t(sg.part_base + k) * a.bm + ri]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    lk[k] = k < int(sg.n_parts) ? a.part_lse[size_t(sg.part_base + k) * a.bm + ri] : -INFINITY;
+    mx = fmaxf(mx, lk[k]);
+  }
+  for (uint32_t k = 4; k < sg.n_parts; ++k) mx = fmaxf(mx, a.part_lse[size_t(sg.part_base + k) * a.bm + ri]);
   float acc[NC];
 #pragma unroll
   for (int e = 0; e < NC; ++e) acc[e] = 0.f;
   float den = 0.f;
   for (uint32_t k = 0; k < sg.n_parts; ++k) {
-    const float l = a.part_lse[size_t(sg.part_base + k) * a.bm + ri];
-    if (!valid || l == -INFINITY) continue;
-    const float w = exp2f(l - mx);
+    const float l = k < 4 ? lk[k & 3] : a.part_lse[size_t(sg.part_base + k) * a.bm + ri];
+    const float w = (valid && l != -INFINITY) ? exp2f(l - mx) : 0.f;  // an empty slot row weighs 0
     den += w;
     const float* src = a.part_o + part_index(sg.part_base + k, a.bm, ri, cd, a.D);
+    float4 v[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+      v[c] = w != 0.f ? *reinterpret_cast<const float4*>(src + size_t(c) * a.bm * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < CPW; ++c) {
-      const float4 v = *reinterpret_cast<const float4*>(src + size_t(c) * a.bm * 4);
-      acc[4 * c] += w * v.x; acc[4 * c + 1] += w * v.y; acc[4 * c + 2] += w * v.z; acc[4 * c + 3] += w * v.w;
+      acc[4 * c] += w * v[c].x; acc[4 * c + 1] += w * v[c].y; acc[4 * c + 2] += w * v[c].z; acc[4 * c + 3] += w * v[c].w;
     }
   }
   __syncthreads();  // u staged
@@ -706,7 +718,14 @@ __global__ void __launch_bounds__(GB_WARPS * 32) gate_block_kernel(GateArgs a) {
 void launch_gate_norm(const GateArgs& a, cudaStream_t s) {
   if (a.rows == 0) return;
   const uint32_t d = a.H * a.D, E = d % 32 == 0 ? d / 32 : 0;
-  if (a.blocks && a.n_blocks && gate_block_supported(a.H, a.D)) {
+  static const bool rows_only = [] {  // MTKV_GATE=row: the row-per-warp kernel everywhere (A/B switch)
+    const char* e = std::getenv("MTKV_GATE");
+    return e && e[0] == 'r';
+  }();
+  // row blocks pay off once there are several per SM (prefill-shaped batches:
+  // 75.6 vs 105.6 us per launch); small decode batches keep one warp per row
+  // (10.7 vs 12.5 us) — ncu launch lists of the configs[1] bench, both policies
+  if (!rows_only && a.blocks && a.n_blocks >= 4 * uint32_t(num_sms()) && gate_block_supported(a.H, a.D)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.n_blocks);
     cfg.blockDim = dim3(GB_WARPS * 32);
