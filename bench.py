@@ -602,6 +602,11 @@ def main():
         cfg["users"] = args.users
     if args.pool_frac:
         cfg["pool_frac"] = args.pool_frac
+        # configs[4]: a pool below two batches of users' pages cannot hold a
+        # batch plus the users still offloading (the reference rejects it), so
+        # small pools serve smaller batches instead of a silently larger pool
+        ppu = -(-(cfg["history"] + 16 * cfg["delta"]) // cfg["page"])
+        cfg["batch"] = max(1, min(cfg["batch"], int(args.pool_frac * cfg["users"] * ppu) // (2 * ppu)))
     world, rank, _ = dist_env()
     if world > 1 or rank != 0:
         args.cpu_baseline = False
