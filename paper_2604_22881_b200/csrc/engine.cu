@@ -640,22 +640,20 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   for (uint32_t r = 0; r < n; ++r) {
     const ReqDev& x = rd[r];
     const ReqWork& R = w.reqs[r];
-    for (uint32_t i = 0; i < x.n_q; ++i) {
-      const uint32_t row = x.q_row0 + i;
-      h_rr[row] = r;
-      h_tok[row] = value_ ? w.tokens[R.tok_off + i] : 0;
-      uint32_t page, slot;
-      if (i < x.n_hist) {
-        const uint64_t pos = x.start + i;
-        page = pages[x.pages_off + uint32_t(pos / S)];
-        slot = uint32_t(pos % S);
-      } else {
-        const uint32_t c = i - x.n_hist;
-        page = pages[x.scratch_off + c / S];
-        slot = c % S;
-      }
-      h_kv[row] = (uint64_t(page) * 2 * S + slot) * d;
+    // per-row metadata, page by page (re-encoded prefixes make batches of ~1e5
+    // rows: one division per page, not per row)
+    std::fill(h_rr + x.q_row0, h_rr + x.q_row0 + x.n_q, r);
+    if (value_) std::memcpy(h_tok + x.q_row0, w.tokens.data() + R.tok_off, size_t(x.n_q) * sizeof(uint32_t));
+    else std::fill(h_tok + x.q_row0, h_tok + x.q_row0 + x.n_q, 0u);
+    for (uint32_t i = 0; i < x.n_hist;) {  // history rows: positions start + i of the user's pages
+      const uint64_t pos = x.start + i;
+      const uint32_t slot0 = uint32_t(pos % S), take = std::min<uint32_t>(S - slot0, x.n_hist - i);
+      const uint64_t base = uint64_t(pages[x.pages_off + uint32_t(pos / S)]) * 2 * S;
+      for (uint32_t j = 0; j < take; ++j) h_kv[x.q_row0 + i + j] = (base + slot0 + j) * d;
+      i += take;
     }
+    for (uint32_t c = 0; c < x.n_cand; ++c)  // candidate rows: the request's scratch pages
+      h_kv[x.q_row0 + x.n_hist + c] = (uint64_t(pages[x.scratch_off + c / S]) * 2 * S + c % S) * d;
     h_last[r] = x.q_row0 + x.n_q - 1;
     nc_k[r] = x.n_cand;
     for (uint32_t c = 0; c < x.n_cand; ++c) {

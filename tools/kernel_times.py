@@ -90,7 +90,7 @@ def main():
     eng = mtkv.Engine(kv, mtkv.CostModel(bus_bandwidth=55e9), mode="hierarchical", backend="value", batch_size=B,
                       model=model, host_reserve_mb=int(1.1 * cfg["users"] * extent_mb) + 1024,
                       host_extent_mb=extent_mb, onload_policy=args.policy)
-    pb = max(1, 65536 // cfg["history"])
+    pb = max(1, min(cfg["batch"], 65536 // cfg["history"]))
     for i in range(0, len(prefill), pb):
         eng.process_batch(prefill[i:i + pb])
     batches = [mtkv.RequestBatch(revisits[i * B:(i + 1) * B]) for i in range(args.warm + args.steps)]

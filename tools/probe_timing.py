@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warm", type=int, default=24)
     ap.add_argument("--config", default="gr4_d256")
-    ap.add_argument("--sequence", default="probe", choices=["probe", "bench"])
+    ap.add_argument("--sequence", default="probe", choices=["probe", "bench", "host"])
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -46,7 +46,7 @@ def main():
                       model=model, host_reserve_mb=int(1.1 * cfg["users"] * extent_mb) + 1024,
                       host_extent_mb=extent_mb, max_users=cfg["users"] + 64, max_user_pages=2 * ppu + 64,
                       onload_policy="adaptive")
-    pb = max(1, 65536 // cfg["history"])
+    pb = max(1, min(B, 65536 // cfg["history"]))
     for i in range(0, len(prefill), pb):
         eng.process_batch(prefill[i:i + pb])
     batches = [revisits[i * B:(i + 1) * B] for i in range(n_b)]
@@ -90,6 +90,36 @@ def main():
         eng.set_onload_policy("adaptive")
         print(json.dumps({"probe": "device", "at": tag, "policy": pol, "req_s": K * B / dt,
                           "ms_per_step": dt / K * 1e3}), flush=True)
+
+    if args.sequence == "host":  # host-side cost per call: packing, submit, rankings, process_batch
+        import numpy as np
+        pk, sb, rk, pbt = [], [], [], []
+        for i in take(K):
+            t0 = time.perf_counter()
+            eng.process_batch(None, packed=packed[i])
+            pbt.append(time.perf_counter() - t0)
+        eng.synchronize()
+        pending = []
+        for i in take(K):
+            t0 = time.perf_counter()
+            rb = mtkv.RequestBatch(batches[i])
+            t1 = time.perf_counter()
+            pending.append(eng.submit(packed=rb))
+            t2 = time.perf_counter()
+            pk.append(t1 - t0)
+            sb.append(t2 - t1)
+            if len(pending) > 2:
+                t3 = time.perf_counter()
+                eng.rankings(pending.pop(0))
+                rk.append(time.perf_counter() - t3)
+        for t in pending:
+            eng.rankings(t)
+        eng.synchronize()
+        ms = lambda v: round(float(np.median(v)) * 1e3, 3)
+        print(json.dumps({"probe": "host_ms_median", "process_batch": ms(pbt), "pack": ms(pk), "submit": ms(sb),
+                          "rankings_wait": ms(rk), "process_batch_p90": round(float(np.percentile(pbt, 90)) * 1e3, 3)}),
+              flush=True)
+        return
 
     if args.sequence == "bench":  # bench.py's phase order: A, B (sync, always, profile), C, E
         device("adaptive", "A")

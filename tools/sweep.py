@@ -43,7 +43,7 @@ def run_mode(cfg: dict, mode: str, steps: int, warm: int, pool_frac: float | Non
     eng = mtkv.Engine(kv, mtkv.CostModel(bus_bandwidth=55e9), mode=mode, backend="value", batch_size=B,
                       model=model, host_reserve_mb=host_mb, host_extent_mb=extent_mb)
     if mode != "recompute":  # recompute keeps no cache: the first visit is not a prefill
-        pb = max(1, 65536 // cfg["history"])
+        pb = max(1, min(cfg["batch"], 65536 // cfg["history"]))
         for i in range(0, len(prefill), pb):
             eng.process_batch(prefill[i:i + pb])
     else:  # the recompute engine still needs each user's token history
