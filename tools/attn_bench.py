@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--tag", default="")
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--prefix", type=int, default=4096, help="cached prefix length (keys) before the revisit spread")
+    ap.add_argument("--nq", type=int, default=72, help="fresh rows per request before the tail (72 = 64 new + 8 cands; "
+                    "4096 with --prefix 0 --tail-frac 0 is a re-encoded history)")
     ap.add_argument("--tail-frac", type=float, default=0.69,
                     help="fraction of requests carrying a recomputed tail (0..127 extra fresh rows)")
     args = ap.parse_args()
@@ -37,9 +39,9 @@ def main():
     L, H, D, S = 4, 2, 128, 32
     d = H * D
     n = args.requests
-    p_pre = (args.prefix + 64 * rng.integers(0, 16, n)).astype(np.uint64)
+    p_pre = (args.prefix + (64 * rng.integers(0, 16, n) if args.prefix else 0 * rng.integers(0, 16, n))).astype(np.uint64)
     tail = np.where(rng.random(n) < args.tail_frac, rng.integers(0, 128, n), 0)
-    n_q = (72 + tail).astype(np.uint32)
+    n_q = (args.nq + tail).astype(np.uint32)
     pages_per = ((p_pre + n_q + S - 1) // S).astype(np.int64)
     P = int(pages_per.sum() + 64)
     perm = rng.permutation(P).astype(np.int32)
@@ -64,7 +66,11 @@ def main():
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     gbs = nbytes / (ms.value / 1e3) / 1e9
-    print(json.dumps({"tag": args.tag, "us_per_launch": ms.value * 1e3, "bytes_per_launch": nbytes,
+    # causal QK^T + PV FLOPs of the visible (query, key) pairs, all heads
+    qpos = [np.arange(int(p), int(p) + int(q)) for p, q in zip(p_pre, n_q)]
+    pairs = int(sum((qp + 1).sum() for qp in qpos))
+    tflops = 4.0 * pairs * d / (ms.value / 1e3) / 1e12
+    print(json.dumps({"tag": args.tag, "us_per_launch": ms.value * 1e3, "bytes_per_launch": nbytes, "tflops": tflops,
                       "rows": rows, "two_tile_requests": int((n_q > 128).sum()), "GBs": gbs, "peak": peak,
                       "frac": gbs / peak, "env": {k: v for k, v in os.environ.items() if k.startswith("MTKV_")}}))
 
