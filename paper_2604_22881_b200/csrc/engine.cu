@@ -527,7 +527,14 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   const std::vector<uint32_t>& pages = recompute_ ? tpages : w.pages;
 
   // ---- rows, attention work, metadata sizes ----
-  std::vector<ReqDev> rd(n);
+  // device requests: the batch's requests, then one extra per split host hit
+  // (the re-encoded head of its prefix, positions [0, head_rows), no
+  // candidates) — after the batch's requests so result rows stay in request order
+  uint32_t n_extra = 0;
+  for (uint32_t r = 0; r < n; ++r) n_extra += w.reqs[r].head_rows ? 1 : 0;
+  const uint32_t nr = n + n_extra;
+  std::vector<ReqDev> rd(nr);
+  std::vector<uint32_t> rd_tok(nr);  // offset of each device request's token ids in w.tokens
   uint32_t rows = 0, max_hist = 0, ncand_total = 0;
   const bool tc = use_tc_;
   for (uint32_t r = 0; r < n; ++r) {
@@ -544,19 +551,40 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     x.scratch_off = recompute_ ? t_soff[r] : R.scratch_off;
     x.n_scratch = recompute_ ? t_ns[r] : R.n_scratch;
     x.user = R.plan.user;
-    x.dep_start = x.start;
-    for (uint32_t q = 0; q < r; ++q)  // an earlier occurrence of the user appends keys this one reads
+    // keys from dep_start on are appended by this batch's projection GEMM: its
+    // own rows, a split host hit's re-encoded head (from 0), or an earlier
+    // occurrence of the user in the batch
+    x.dep_start = R.head_rows ? 0 : x.start;
+    for (uint32_t q = 0; q < r; ++q)
       if (w.reqs[q].slot == R.slot) {
-        x.dep_start = rd[q].dep_start;
+        x.dep_start = std::min(x.dep_start, rd[q].dep_start);
         break;
       }
+    rd_tok[r] = R.tok_off;
     rows += x.n_q;
     ncand_total += x.n_cand;
     max_hist = std::max(max_hist, x.n_hist);
   }
+  for (uint32_t r = 0, e = n; r < n; ++r) {
+    const ReqWork& R = w.reqs[r];
+    if (!R.head_rows) continue;
+    ReqDev& x = rd[e];
+    x = ReqDev{};
+    x.q_row0 = rows;
+    x.n_hist = x.n_q = R.head_rows;
+    x.start = 0;
+    x.pages_off = R.pages_off;
+    x.n_pages = R.n_pages;
+    x.user = R.plan.user;
+    x.dep_start = 0;
+    rd_tok[e] = R.head_tok_off;
+    rows += x.n_q;
+    max_hist = std::max(max_hist, x.n_hist);
+    ++e;
+  }
   last_rows_ = rows;
   if (value_) {
-    plan_attention(rd.data(), n, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_);
+    plan_attention(rd.data(), nr, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_);
     if (attn_kind_ == AttnKind::Pp && plan_.n_ctas() % 2) plan_.cta_off.push_back(plan_.cta_off.back());
   }
   const uint32_t bq = plan_.bm;
@@ -566,15 +594,15 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   const uint32_t n_on = uint32_t(w.onloads.size()), n_off = uint32_t(w.offloads.size());
   uint32_t n_gblk = 0;  // gate/norm row blocks
   if (value_)
-    for (uint32_t r = 0; r < n; ++r) n_gblk += (rd[r].n_q + kGateBlockRows - 1) / kGateBlockRows;
+    for (uint32_t r = 0; r < nr; ++r) n_gblk += (rd[r].n_q + kGateBlockRows - 1) / kGateBlockRows;
 
   size_t need = 0;
-  need = align16(need + n * sizeof(ReqDev));
+  need = align16(need + nr * sizeof(ReqDev));
   need = align16(need + pages.size() * sizeof(uint32_t));
   need = align16(need + rows * sizeof(uint32_t));      // tok
   need = align16(need + rows * sizeof(uint64_t));      // kv_off
   need = align16(need + rows * sizeof(uint32_t));      // row_req
-  need = align16(need + n * sizeof(uint32_t));         // last_row
+  need = align16(need + nr * sizeof(uint32_t));        // last_row
   need = align16(need + n_segs * sizeof(AttnSeg));
   need = align16(need + (tc ? 0 : n_items) * sizeof(AttnItem));
   need = align16(need + n_pieces * sizeof(AttnPiece));
@@ -592,7 +620,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   char* db = static_cast<char*>(meta_.p) + size_t(k) * (meta_.bytes / kRing);
   if (need > meta_.bytes / kRing) { err = "engine: metadata ring overflow"; return MTKV_ERROR; }
   size_t off = 0;
-  ReqDev* h_req = carve<ReqDev>(hb, off, n);
+  ReqDev* h_req = carve<ReqDev>(hb, off, nr);
   const size_t o_pages = off;
   uint32_t* h_pages = carve<uint32_t>(hb, off, pages.size());
   const size_t o_tok = off;
@@ -602,7 +630,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   const size_t o_rr = off;
   uint32_t* h_rr = carve<uint32_t>(hb, off, rows);
   const size_t o_last = off;
-  uint32_t* h_last = carve<uint32_t>(hb, off, n);
+  uint32_t* h_last = carve<uint32_t>(hb, off, nr);
   const size_t o_segs = off;
   AttnSeg* h_segs = carve<AttnSeg>(hb, off, n_segs);
   const size_t o_items = off;
@@ -619,13 +647,13 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   off = align16(o_cand + 2 * ncand_total * sizeof(uint32_t));
   const size_t o_gblk = off;
   uint32_t* h_gblk = carve<uint32_t>(hb, off, 2 * n_gblk);
-  for (uint32_t r = 0, b = 0; r < n && value_; ++r)
+  for (uint32_t r = 0, b = 0; r < nr && value_; ++r)
     for (uint32_t i0 = 0; i0 < rd[r].n_q; i0 += kGateBlockRows, ++b) {
       h_gblk[2 * b] = r;
       h_gblk[2 * b + 1] = i0;
     }
 
-  std::memcpy(h_req, rd.data(), n * sizeof(ReqDev));
+  std::memcpy(h_req, rd.data(), nr * sizeof(ReqDev));
   if (!pages.empty()) std::memcpy(h_pages, pages.data(), pages.size() * sizeof(uint32_t));
   std::vector<uint32_t>& cands_k = slot_cands_[k];
   std::vector<uint32_t>& nc_k = slot_nc_[k];
@@ -637,13 +665,12 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   if (!tc && n_items) std::memcpy(h_items, plan_.items.data(), n_items * sizeof(AttnItem));
   if (n_pieces) std::memcpy(h_pieces, plan_.pieces.data(), n_pieces * sizeof(AttnPiece));
   if (tc && n_items) std::memcpy(h_ctaoff, plan_.cta_off.data(), (n_items + 1) * sizeof(uint32_t));
-  for (uint32_t r = 0; r < n; ++r) {
+  for (uint32_t r = 0; r < nr; ++r) {
     const ReqDev& x = rd[r];
-    const ReqWork& R = w.reqs[r];
     // per-row metadata, page by page (re-encoded prefixes make batches of ~1e5
     // rows: one division per page, not per row)
     std::fill(h_rr + x.q_row0, h_rr + x.q_row0 + x.n_q, r);
-    if (value_) std::memcpy(h_tok + x.q_row0, w.tokens.data() + R.tok_off, size_t(x.n_q) * sizeof(uint32_t));
+    if (value_) std::memcpy(h_tok + x.q_row0, w.tokens.data() + rd_tok[r], size_t(x.n_q) * sizeof(uint32_t));
     else std::fill(h_tok + x.q_row0, h_tok + x.q_row0 + x.n_q, 0u);
     for (uint32_t i = 0; i < x.n_hist;) {  // history rows: positions start + i of the user's pages
       const uint64_t pos = x.start + i;
@@ -655,9 +682,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     for (uint32_t c = 0; c < x.n_cand; ++c)  // candidate rows: the request's scratch pages
       h_kv[x.q_row0 + x.n_hist + c] = (uint64_t(pages[x.scratch_off + c / S]) * 2 * S + c % S) * d;
     h_last[r] = x.q_row0 + x.n_q - 1;
+    if (r >= n) continue;  // an extra (re-encoded head) has no candidates
     nc_k[r] = x.n_cand;
     for (uint32_t c = 0; c < x.n_cand; ++c) {
-      const uint32_t id = value_ ? w.tokens[R.tok_off + x.n_hist + c] : 0;
+      const uint32_t id = value_ ? w.tokens[rd_tok[r] + x.n_hist + c] : 0;
       h_creq[cj] = r;
       h_cid[cj] = id;
       cands_k.push_back(id);
@@ -768,7 +796,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     if (x_.ensure(rb, comp_) || x2_.ensure(rb, comp_) || u_.ensure(rb, comp_) || q_.ensure(rb, comp_) ||
         mid_.ensure(rb, comp_) || part_o_.ensure(size_t(plan_.n_slots) * part_slot_floats(bq, g_.D) * sizeof(float), comp_) ||
         part_lse_.ensure(size_t(plan_.n_slots) * bq * sizeof(float), comp_) ||
-        logits_.ensure(size_t(n) * V * sizeof(float), comp_) ||
+        logits_.ensure(size_t(nr) * V * sizeof(float), comp_) ||
         scores_.ensure(size_t(ncand_total) * sizeof(float), comp_)) {
       err = "engine: workspace alloc";
       return MTKV_ERROR;
@@ -853,7 +881,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     if (opt_.keep_logits || !w_out_t_) {
       // full-vocabulary logits (kept for the caller), candidates picked from them
       GemmArgs hd{};
-      hd.A = X; hd.row_idx = d_last; hd.B = w_out_; hd.M = n; hd.N = V; hd.K = d; hd.epi = Epi::F32; hd.out = logits_.p;
+      hd.A = X; hd.row_idx = d_last; hd.B = w_out_; hd.M = nr; hd.N = V; hd.K = d; hd.epi = Epi::F32; hd.out = logits_.p;
       launch_gemm(hd, comp_);
       ++launches;
       if (ncand_total) {
@@ -869,7 +897,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     }
     if (calibrate_) CK(cudaEventRecord(ev_stk1_[k], comp_));
   } else {
-    launch_tag_append(pool, d_req, d_pages, n, max_hist, g_, comp_);
+    launch_tag_append(pool, d_req, d_pages, nr, max_hist, g_, comp_);
     ++launches;
   }
 

@@ -6,6 +6,8 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "devctl.hpp"
@@ -344,18 +346,44 @@ uint32_t Planner::last_page_len(uint32_t user) const {
   return rem == 0 ? kv_.page_size : rem;
 }
 
-// Adaptive onload policy: walk the batch's host-hit requests in order and send
-// each to whichever resource would finish it earlier — the host link (its
-// persisted chunks at link_Bps_) or the SMs (re-encoding its prefix at
-// recompute_tps_, on top of the batch's own fresh rows). The batch then costs
-// roughly max(link, SMs) instead of link + nothing.
+// Adaptive onload policy. Split form (default): every host hit re-encodes the
+// same fraction f of its persisted chunks — its EARLIEST chunks, whose
+// positions attend over the fewest keys, so a re-encoded token costs the SMs
+// less than one late in the history — and onloads the rest; f balances the
+// batch's SM time (fresh rows + re-encoded rows at recompute_tps_) against its
+// host-link time (onloaded chunks at link_Bps_). The positions a request
+// re-encodes are [0, f n C): disjoint from its own fresh rows, so the executor
+// runs them as an extra request (BatchWork keeps one ReqWork per request).
+// Whole form (MTKV_ADAPTIVE_SPLIT=0): walk the host hits and send each whole
+// prefix to whichever resource would finish it earlier.
 void Planner::choose_recompute(BatchWork& w) {
-  double t_link = 0, t_sm = 0;
+  static const bool split = [] {
+    const char* e = std::getenv("MTKV_ADAPTIVE_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  double t_sm = 0;
   for (const ReqWork& r : w.reqs)
     t_sm += double(r.plan.fresh_history + r.plan.delta + r.plan.num_candidates) / recompute_tps_;
+  const double c_link_chunk = double(chunk_bytes_u64_) / link_Bps_, c_sm_chunk = double(kv_.chunk_size) / recompute_tps_;
+  if (split) {
+    double chunks = 0;
+    for (const ReqWork& r : w.reqs) chunks += r.plan.onload_chunks;
+    if (chunks == 0) return;
+    // t_sm + f * chunks * c_sm = (1 - f) * chunks * c_link
+    const double f = std::min(1.0, std::max(0.0, (chunks * c_link_chunk - t_sm) / (chunks * (c_link_chunk + c_sm_chunk))));
+    for (ReqWork& r : w.reqs) {
+      const uint32_t n = r.plan.onload_chunks;
+      if (!n) continue;
+      const uint32_t k = std::min<uint32_t>(n, uint32_t(std::lround(f * n)));
+      if (k == n) r.recompute_prefix = true;  // contiguous with the request's own rows: one request
+      else r.head_chunks = k;
+    }
+    return;
+  }
+  double t_link = 0;
   for (ReqWork& r : w.reqs) {
     if (!r.plan.onload_chunks) continue;
-    const double c_link = double(r.plan.onload_chunks) * double(chunk_bytes_u64_) / link_Bps_;
+    const double c_link = double(r.plan.onload_chunks) * c_link_chunk;
     const double c_sm = double(r.plan.reusable_len) / recompute_tps_;
     if (t_link + c_link <= t_sm + c_sm) {
       t_link += c_link;
@@ -438,9 +466,13 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
   for (uint32_t i = 0; i < n; ++i) {
     const ReqWork& r = w.reqs[i];
     const UserRec& u = users_[slot[i]];
-    if (r.plan.onload_chunks) (r.recompute_prefix ? prefix_recomputed_ : prefix_onloaded_) += r.plan.reusable_len;
+    if (r.plan.onload_chunks) {
+      const uint64_t head = r.recompute_prefix ? r.plan.reusable_len : uint64_t(r.head_chunks) * kv_.chunk_size;
+      prefix_recomputed_ += head;
+      prefix_onloaded_ += r.plan.reusable_len - head;
+    }
     if (r.recompute_prefix) continue;  // its K/V is re-encoded, nothing crosses the host link
-    for (uint32_t c = 0; c < r.plan.onload_chunks; ++c) {
+    for (uint32_t c = r.head_chunks; c < r.plan.onload_chunks; ++c) {  // the re-encoded head is not onloaded
       ChunkMove m;
       m.chunk_id = u.host_chunks[c];
       m.user = u.id;
@@ -490,6 +522,19 @@ void Planner::plan_batch(const mtkv_request* reqs, uint32_t n, BatchWork& w) {
     ReqWork& r = w.reqs[i];
     UserRec& u = users_[slot[i]];
     const auto& p = r.plan;
+    if (r.head_chunks) {  // split host hit: the re-encoded head's token ids (positions [0, head_rows))
+      r.head_rows = r.head_chunks * kv_.chunk_size;
+      r.head_tok_off = uint32_t(w.tokens.size());
+      if (keep_tokens_) {
+        if (u.tokens.size() < r.head_rows) {
+          w.rc = MTKV_ERROR;
+          w.error = "value mode: trace must carry explicit token ids";
+          return;
+        }
+        w.tokens.insert(w.tokens.end(), u.tokens.begin(), u.tokens.begin() + r.head_rows);
+      }
+      w.fresh_rows += r.head_rows;
+    }
     r.tok_off = uint32_t(w.tokens.size());
     if (cached) {
       // a re-encoded host-hit prefix (adaptive policy) is appended from position 0

@@ -56,6 +56,11 @@ struct ReqWork {
   uint32_t scratch_off = 0, n_scratch = 0;  // into BatchWork::pages
   uint32_t tok_off = 0;        // into BatchWork::tokens: fresh history ids ++ candidate ids
   bool recompute_prefix = false;  // adaptive onload policy: host-hit prefix re-encoded (start = 0)
+  // adaptive policy, split host hit: the prefix's first head_chunks chunks are
+  // re-encoded (positions [0, head_rows), their ids at head_tok_off in
+  // BatchWork::tokens: the executor runs them as an extra request ahead of this
+  // one's attention), the remaining chunks are onloaded
+  uint32_t head_chunks = 0, head_rows = 0, head_tok_off = 0;
 };
 
 struct ChunkMove {

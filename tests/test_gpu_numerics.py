@@ -22,6 +22,8 @@
   ~1e-44 (below fp32's normal range), so L = 4 checks the K/V and L = 3 the
   logits (see the test's docstring).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -35,8 +37,11 @@ pytestmark = pytest.mark.gpu
 ATTN_REL = 1e-2
 LOGIT_REL = 0.03
 KV_REL = 0.03
-MODE_REL = 1e-2        # modes against each other: K/V in the pool
-MODE_REL_LOGIT = 2e-2  # and logits (bf16 roundings of differently materialised prefixes compound per layer)
+MODE_REL = float(os.environ.get("MTKV_TEST_MODE_REL", 2e-2))  # modes against each other: K/V in the pool ...
+MODE_REL_LOGIT = 2e-2  # ... and logits. The modes run different batch shapes, so shape-dependent kernel
+# choices (row-block vs row-per-warp gate/norm) reduce in different fp32 orders; their bf16 roundings
+# compound per layer of this (degenerate, eps-dominated layer-norm) model: measured K/V 1.6e-2 with the
+# shape-dependent gate/norm, 4.8e-4 with MTKV_GATE=row everywhere; logits 0.8-1.2e-2.
 POISON_K, POISON_V = 30.0, 1000.0
 
 
@@ -255,3 +260,19 @@ def test_two_lane_attention_kernel_same_bars():
                        env={**os.environ, "MTKV_ATTN": "pp"}, capture_output=True, text=True, timeout=600)
     print(r.stdout[-400:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_modes_agree_to_bf16_noise_on_one_kernel_path():
+    """With the same gate/norm kernel for every batch shape (MTKV_GATE=row), the
+    four executor modes' resident K/V agree to bf16 rounding noise (<= 1e-3;
+    measured 4.5e-4 .. 5.1e-4, incl. the adaptive policy's split re-encode): the
+    modes differ only in how a prefix is materialised, not in the math."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_numerics.py"), "-q", "-x", "-s",
+                        "-p", "no:cacheprovider", "-k", "configs1_dims and 4"],
+                       env={**os.environ, "MTKV_GATE": "row", "MTKV_TEST_MODE_REL": "1e-3"},
+                       capture_output=True, text=True, timeout=900)
+    print("\n".join(l for l in r.stdout.splitlines() if "invariance" in l))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
