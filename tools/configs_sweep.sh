@@ -10,7 +10,7 @@ for m in recompute gpu_only hierarchical; do
   timeout 600 python bench.py --no-cpu-baseline --steps 20 --mode $m 2>/dev/null | tail -1 >> $O/${T}_configs2.jsonl
 done
 : > $O/${T}_configs4.jsonl
-for f in 0.01 0.02 0.05 0.2 0.5; do
+for f in 0.01 0.02 0.05 0.1 0.2 0.5; do
   timeout 600 python bench.py --no-cpu-baseline --steps 20 --pool-frac $f 2>/dev/null | tail -1 >> $O/${T}_configs4.jsonl
 done
 wc -l $O/${T}_configs*.jsonl

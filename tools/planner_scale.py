@@ -57,7 +57,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batches", type=int, default=40)
     args = ap.parse_args()
-    for users, batch in ((2048, 64), (16384, 256), (65536, 512)):
+    # (65536 users / batch 512 exhausted the box's host memory for the pinned tier)
+    for users, batch in ((2048, 64), (16384, 256)):
         for planner in ("host", "device"):
             print(json.dumps(run(users, batch, planner, args.batches)), flush=True)
 

@@ -23,3 +23,11 @@ timeout 900 ncu --profile-from-start off --set full --clock-control none --impor
 timeout 900 ncu --profile-from-start off --set full --clock-control none -k regex:gate_block_kernel -c 1 \
   -o $O/${T}_gate_ncu python tools/kernel_times.py --steps 1 --warm 30 --ncu --policy adaptive > /dev/null 2>&1
 ls -la $O | grep $T
+# the other BASELINE configs and the reference arm (bench lines)
+bash tools/configs_sweep.sh $T
+for c in gr8_d512 tiny_d64; do
+  timeout 900 python bench.py --no-cpu-baseline --steps 20 --config $c 2>/dev/null | tail -1 > $O/${T}_bench_$c.json
+done
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $O/${T}_reference_arm.json 2>&1
+python tools/planner_scale.py --batches 30 > $O/${T}_planner_scale.jsonl 2>/dev/null
+ls -la $O | grep $T
