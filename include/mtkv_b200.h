@@ -158,6 +158,12 @@ mtkv_planner* mtkv_planner_create(const mtkv_kv_config* kv, const mtkv_cost_mode
 void mtkv_planner_destroy(mtkv_planner* p);
 int mtkv_planner_process_batch(mtkv_planner* p, const mtkv_request* reqs, uint32_t n);
 int mtkv_planner_drain(mtkv_planner* p);
+/* The executor's host-hit policy as the planner applies it (mtkv_engine_options::
+ * onload_policy, fixed rates: the engine measures them instead when given 0):
+ * which host-hit prefix chunks a batch re-encodes and which it onloads (the
+ * report's prefix_recomputed / prefix_onloaded). Control-plane decisions are
+ * the same under every policy. */
+int mtkv_planner_set_onload_policy(mtkv_planner* p, uint32_t policy, double onload_gbs, double recompute_mtok_s);
 /* CacheManager step surface (manager.hpp:89-147) on the same host control
  * plane, for callers that drive the manager themselves the way
  * Engine<B>::process_batch does (sim.hpp:332-455). Request indices refer to the

@@ -125,6 +125,7 @@ EXPORTED_SYMBOLS = [
     "mtkv_kv_config_default", "mtkv_kv_config_validate", "mtkv_parse_config_text",
     "mtkv_cost_model_default", "mtkv_pages_needed", "mtkv_persisted_prefix", "mtkv_last_error",
     "mtkv_planner_create", "mtkv_planner_destroy", "mtkv_planner_process_batch", "mtkv_planner_drain",
+    "mtkv_planner_set_onload_policy",
     "mtkv_planner_prepare_metadata", "mtkv_planner_scratch_pages", "mtkv_planner_release_scratch",
     "mtkv_planner_commit_onload", "mtkv_planner_finish_append", "mtkv_planner_advance_persisted",
     "mtkv_planner_lock_user", "mtkv_planner_unlock_user", "mtkv_planner_last_page_len",
@@ -170,6 +171,7 @@ def lib():
         "mtkv_planner_destroy": (None, [vp]),
         "mtkv_planner_process_batch": (C.c_int, [vp, C.POINTER(_Request), u32]),
         "mtkv_planner_drain": (C.c_int, [vp]),
+        "mtkv_planner_set_onload_policy": (C.c_int, [vp, C.c_uint32, C.c_double, C.c_double]),
         "mtkv_engine_create": (vp, [C.POINTER(_KV), C.POINTER(_Cost), C.POINTER(_EngineOpts)]),
         "mtkv_engine_destroy": (None, [vp]),
         "mtkv_engine_process_batch": (C.c_int, [vp, C.POINTER(_Request), u32]),
@@ -496,6 +498,13 @@ class Planner(_ManagerView):
 
     def drain(self) -> None:
         _check(lib().mtkv_planner_drain(self._h))
+
+    def set_onload_policy(self, policy: str, onload_gbs: float, recompute_mtok_s: float) -> None:
+        """The executor's host-hit split as the planner applies it at fixed rates
+        (report: prefix_recomputed / prefix_onloaded); decisions are unchanged."""
+        if policy not in ("always", "adaptive"):
+            raise Error(f"unknown onload policy {policy!r}")
+        _check(lib().mtkv_planner_set_onload_policy(self._h, int(policy == "adaptive"), onload_gbs, recompute_mtok_s))
 
 
 class Ticket:

@@ -158,6 +158,14 @@ int mtkv_planner_drain(mtkv_planner* p) {
   return MTKV_OK;
 }
 
+int mtkv_planner_set_onload_policy(mtkv_planner* p, uint32_t policy, double onload_gbs, double recompute_mtok_s) {
+  if (!p) return fail(MTKV_ERROR, "planner: null handle");
+  if (policy > MTKV_ONLOAD_ADAPTIVE || onload_gbs <= 0 || recompute_mtok_s <= 0)
+    return fail(MTKV_ERROR, "planner: onload policy needs a known policy and positive rates");
+  p->p.set_onload_policy(int(policy), onload_gbs * 1e9, recompute_mtok_s * 1e6);
+  return MTKV_OK;
+}
+
 int mtkv_planner_prepare_metadata(mtkv_planner* p, const mtkv_request* reqs, uint32_t n, int host_enabled) {
   std::string err;
   const int rc = p->p.mgr_prepare(reqs, n, host_enabled != 0, err);

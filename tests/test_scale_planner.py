@@ -65,3 +65,41 @@ def test_host_planner_replays_reference_at_scale(name, pick):
         replay(p, st.split(trace, run["batch_size"], sizes), run)
         ran += 1
     assert ran > 0
+
+
+@pytest.mark.parametrize("split_gbs", [(54.0, 30.0), (54.0, 3.0), (5.0, 300.0)], ids=["balanced", "slow_sms", "slow_link"])
+def test_adaptive_split_keeps_reference_decisions(split_gbs):
+    """The adaptive host-hit policy (planner.cpp choose_recompute, split form)
+    re-encodes the earliest chunks of every host hit and onloads the rest: the
+    reference's state chain, final state and report must be untouched (the same
+    fixture as the 'always' replay), every host-hit prefix token must be either
+    re-encoded or onloaded, chunk-aligned, and the split must follow the rates
+    (slow SMs -> mostly onloaded, slow link -> mostly re-encoded)."""
+    gbs, mtok = split_gbs
+    case = scale_case("scale_bench_c1")
+    trace, sizes = st.build(case["trace"])
+    run = [r for r in case["runs"] if r["mode"] == "hierarchical"][0]
+    always = mtkv.Planner(_kv(case, run), mtkv.CostModel(**case["cost"]), mode="hierarchical")
+    adaptive = mtkv.Planner(_kv(case, run), mtkv.CostModel(**case["cost"]), mode="hierarchical")
+    adaptive.set_onload_policy("adaptive", gbs, mtok)
+    replay(adaptive, st.split(trace, run["batch_size"], sizes), run)  # bit-exact to the reference
+    for b in st.split(trace, run["batch_size"], sizes):
+        try:
+            always.process_batch(b)
+        except mtkv.BatchRejected:
+            pass
+    always.drain()
+    ra, rb = always.report(), adaptive.report()
+    chunk = case["kv"].get("chunk_size", mtkv.KVConfig().chunk_size)
+    total = ra["prefix_onloaded"]
+    assert ra["prefix_recomputed"] == 0 and total > 0
+    assert rb["prefix_recomputed"] + rb["prefix_onloaded"] == total
+    assert rb["prefix_recomputed"] % chunk == 0 and rb["prefix_onloaded"] % chunk == 0
+    frac = rb["prefix_recomputed"] / total
+    print(f"link {gbs} GB/s, SMs {mtok} M tok/s: re-encoded fraction {frac:.3f}")
+    if mtok <= 3.0:
+        assert frac < 0.2
+    elif gbs <= 5.0:
+        assert frac > 0.8
+    else:
+        assert 0.0 < frac < 1.0
