@@ -405,7 +405,9 @@ __global__ void __launch_bounds__(gps::THREADS, 1)
 #pragma unroll
       for (int rr = int(lane) / CPR; rr < 32; rr += 32 / CPR) {
         const int row = m0 + int(q) * 32 + rr;
-        const uint64_t kvo = __shfl_sync(0xffffffffu, kv_lane, rr);  // every lane: no early exit before it
+        // K / V parts: the row's pool offset from the lane that loaded it (part is
+        // warp-uniform; every lane reaches the shuffle: no early exit before it)
+        const uint64_t kvo = part >= 2 ? __shfl_sync(0xffffffffu, kv_lane, rr) : 0;
         if (row >= g.M) continue;
         const uint4 val = stg[rr * CPR + (ck ^ ((rr >> 1) & (CPR - 1)))];
         __nv_bfloat16* dst;
