@@ -19,18 +19,27 @@ N > 1: launched by torchrun, one process per GPU; users are sharded by
 user-id hash (paper_2604_22881_b200.shard.shard_of), each rank owns an
 independent cache shard; no collective on the data path ("scaling": "weak").
 
+Host hits are executed with the `adaptive` policy by default (`--onload-policy
+always` is the reference's executor): every host hit re-encodes its earliest
+chunks on the SMs and onloads the rest, balanced at measured rates; the
+control plane, hit ratios and simulated clock are the reference's under both
+("Host-hit executor policy"); phase E reports the other policy.
+
 Phases: A = device throughput (`value`, pre-packed requests, CUDA events);
-B = per-batch latency (p50/p99) with per-kernel CUDA-event timing of the
-attention launches (`roofline`) and the KV scatter/gather (`other_kernels`);
+B = per-batch latency (p50/p99, `always` policy) with per-kernel CUDA-event
+timing of the attention launches (`roofline`: the decode-shaped incremental
+attention), the projection GEMM and the KV scatter/gather (`other_kernels`);
 C = end to end through the public API (`e2e`: Python request dicts -> C-ABI,
-pipelined submit / rankings read-back of every batch); D (untimed) = 8 more
-batches under CUPTI for `overlap` (fraction of kernel time with an H2D copy in
-flight, H2D engine busy fraction). Also reported:
-`host_link` (H2D GB/s vs the measured pinned-copy peak), `control_plane`
-(planning cost; `--planner device` runs the GPU control plane), `cpu_baseline`
-(the unmodified reference on this box's host cores). Other BASELINE configs:
-`--config gr8_d512` (configs[3] per-GPU shard), `tools/sweep.py ablation|pressure`
-(configs[2], configs[4]).
+pipelined submit / rankings read-back of every batch, 3 batches in flight);
+D (untimed) = 8 more batches under CUPTI for `overlap` (fraction of kernel
+time with an H2D copy in flight, H2D engine busy fraction) and the copy
+kernels' own durations; E = the other host-hit policy on the next K batches.
+Also reported: `host_link` (H2D GB/s vs the measured pinned-copy peak),
+`control_plane` (planning cost; `--planner device` runs the GPU control
+plane), `cpu_baseline` (the unmodified reference on this box's host cores).
+Other BASELINE configs: `--config gr8_d512` (configs[3] per-GPU shard),
+`--config tiny_d64` (configs[0]), `--mode recompute|gpu_only` (configs[2]),
+`--pool-frac F` (configs[4]); tools/configs_sweep.sh runs them.
 """
 from __future__ import annotations
 
