@@ -134,6 +134,13 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout: float = 5.0):
+        """nvidia-smi's start-up (NVML init) can hold the driver for up to ~1 s:
+        let it finish before a timed region starts (sampling continues inside it)."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -311,6 +318,7 @@ def run_b200(args, cfg):
     l0 = eng.kernel_launches()
     clocks = Clocks(local)
     clocks.start()
+    clocks.wait_first()
     torch.cuda.synchronize()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
