@@ -76,6 +76,12 @@ CONFIGS = {
 }
 
 
+def LAST_LAYER_REDUCED(cfg) -> bool:
+    """The engine's tcgen05 attention path (head_dim 64/128, not forced to another
+    kernel by MTKV_ATTN) runs the last layer for each request's last row only."""
+    return cfg["D"] in (64, 128) and os.environ.get("MTKV_ATTN", "") not in ("mma", "pp")
+
+
 CONFIG_TAG = {"gr4_d256": "configs[1]", "tiny_d64": "configs[0]", "gr8_d512": "configs[3]"}
 
 
@@ -366,8 +372,11 @@ def run_b200(args, cfg):
         for p in eng.plans():
             keys = p["history_len"] + p["delta"] + p["num_candidates"]
             rows = p["fresh_history"] + p["delta"] + p["num_candidates"]
-            # per layer: K+V of every visible key once + Q (bf16) read + O (fp32) write
-            attn_bytes += cfg["L"] * (keys * d * 2 * 2 + rows * d * 2 + rows * d * 4)
+            # per layer: K+V of every visible key once + Q (bf16) read + O (fp32) write;
+            # the last layer computes only each request's last row (tcgen05 path)
+            last_rows = 1 if LAST_LAYER_REDUCED(cfg) else rows
+            attn_bytes += (cfg["L"] - 1) * (keys * d * 2 * 2 + rows * d * 2 + rows * d * 4)
+            attn_bytes += keys * d * 2 * 2 + last_rows * d * 6
     eng.set_profile(False)
     eng.set_onload_policy(args.onload_policy)
     phase_b = _phase(rb0, eng.report(), K, B)

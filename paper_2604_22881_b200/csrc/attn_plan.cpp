@@ -33,14 +33,14 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
     uint64_t total = 0;
     for (uint32_t r = 0; r < n; ++r) {
       ReqDev& R = reqs[r];
-      R.qtiles = (R.n_q + kTcBM - 1) / kTcBM;
+      R.qtiles = (R.n_q - R.q_skip + kTcBM - 1) / kTcBM;
       R.seg0 = uint32_t(P.segs.size());
       R.split_keys = 0;
       // logical key space: user keys [0, KA) padded to a page boundary, then candidates
       const uint64_t KA = R.start + R.n_hist, KAp = (KA + S - 1) / S * S;
       for (uint32_t h = 0; h < H; ++h)
         for (uint32_t qt = 0; qt < R.qtiles; ++qt) {
-          const uint64_t q_end = std::min<uint64_t>(R.n_q, uint64_t(qt + 1) * kTcBM);
+          const uint64_t q_end = std::min<uint64_t>(R.n_q, R.q_skip + uint64_t(qt + 1) * kTcBM);
           const uint64_t pos_last = R.start + q_end - 1;
           const uint64_t k_vis = pos_last >= KA ? KAp + (pos_last - KA + 1) : pos_last + 1;
           const uint32_t nt = uint32_t((k_vis + kTcBN - 1) / kTcBN);
@@ -138,6 +138,7 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
       pc.pages_off = R.pages_off;
       pc.scratch_off = R.scratch_off;
       pc.n_scratch = R.n_scratch;
+      pc.q_skip = R.q_skip;
       pc.start = R.start;
       pc.dep_start = R.dep_start;
     }

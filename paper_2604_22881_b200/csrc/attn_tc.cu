@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) {
 #pragma unroll
           for (int b = 0; b < NB; ++b)
-            tma_load_2d(dst + b * QBLK, &q_map, int(col + 64 * b), int(P.q_row0 + P.qtile * BM), &full[st]);
+            tma_load_2d(dst + b * QBLK, &q_map, int(col + 64 * b), int(P.q_row0 + P.q_skip + P.qtile * BM), &full[st]);
         }
         advance();
       }
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(384, 1)
       const AttnPiece P = a.pieces[pc];
       const uint64_t KA = P.start + P.n_hist;
       const uint64_t KAp = (KA + S - 1) / S * S;
-      const uint32_t q0 = P.qtile * BM;
+      const uint32_t q0 = P.q_skip + P.qtile * BM;
       const uint32_t q_end = min(P.n_q, q0 + BM);
       const uint64_t pos_last = P.start + q_end - 1;
       const uint64_t k_vis = pos_last >= KA ? KAp + (pos_last - KA + 1) : pos_last + 1;

@@ -587,6 +587,27 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     plan_attention(rd.data(), nr, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_);
     if (attn_kind_ == AttnKind::Pp && plan_.n_ctas() % 2) plan_.cta_off.push_back(plan_.cta_off.back());
   }
+  // Last layer: the head reads only each request's last row (model.cpp:195
+  // logits = e[last] W_out), so after the projection GEMM (which still appends
+  // every fresh row's K/V of that layer) the attention, gate/norm and MLP run
+  // for one row per request — none for a split host hit's re-encoded head.
+  // rd_last: the requests with q_skip = n_q - 1; rd_gate: the same segments seen
+  // from compact rows (row r = request r).
+  const bool reduce_last = value_ && attn_kind_ == AttnKind::Tc;
+  std::vector<ReqDev> rd_last, rd_gate;
+  if (reduce_last) {
+    rd_last.assign(rd.begin(), rd.begin() + n);
+    for (ReqDev& x : rd_last) x.q_skip = x.n_q - 1;
+    plan_attention(rd_last.data(), n, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_last_);
+    rd_gate = rd_last;
+    for (uint32_t r = 0; r < n; ++r) {
+      rd_gate[r].q_row0 = r;
+      rd_gate[r].n_q = 1;
+    }
+  }
+  const uint32_t n_segs_l = reduce_last ? uint32_t(plan_last_.segs.size()) : 0;
+  const uint32_t n_items_l = reduce_last ? plan_last_.n_ctas() : 0;
+  const uint32_t n_pieces_l = reduce_last ? uint32_t(plan_last_.pieces.size()) : 0;
   const uint32_t bq = plan_.bm;
   const uint32_t n_segs = value_ ? uint32_t(plan_.segs.size()) : 0;
   const uint32_t n_items = value_ ? (tc ? plan_.n_ctas() : uint32_t(plan_.items.size())) : 0;
@@ -610,6 +631,14 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   need = align16(need + (n_on + n_off) * sizeof(ChunkWork));
   need = align16(need + 2 * ncand_total * sizeof(uint32_t));
   need = align16(need + 2 * n_gblk * sizeof(uint32_t));
+  if (reduce_last) {
+    need = align16(need + n * sizeof(ReqDev));              // rd_last
+    need = align16(need + n * sizeof(ReqDev));              // rd_gate
+    need = align16(need + n_segs_l * sizeof(AttnSeg));
+    need = align16(need + n_pieces_l * sizeof(AttnPiece));
+    need = align16(need + (n_items_l + 1) * sizeof(uint32_t));
+    need = align16(need + 2 * n * sizeof(uint32_t));        // identity rows, u rows
+  }
   if (meta_host_bytes_[k] < need) {
     if (meta_host_[k]) cudaFreeHost(meta_host_[k]);
     meta_host_bytes_[k] = std::max(need, meta_host_bytes_[k] * 2);
@@ -653,6 +682,26 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       h_gblk[2 * b + 1] = i0;
     }
 
+  size_t o_req_l = 0, o_req_g = 0, o_segs_l = 0, o_pieces_l = 0, o_ctaoff_l = 0, o_rowc = 0;
+  if (reduce_last) {
+    o_req_l = off;
+    std::memcpy(carve<ReqDev>(hb, off, n), rd_last.data(), n * sizeof(ReqDev));
+    o_req_g = off;
+    std::memcpy(carve<ReqDev>(hb, off, n), rd_gate.data(), n * sizeof(ReqDev));
+    o_segs_l = off;
+    std::memcpy(carve<AttnSeg>(hb, off, n_segs_l), plan_last_.segs.data(), n_segs_l * sizeof(AttnSeg));
+    o_pieces_l = off;
+    std::memcpy(carve<AttnPiece>(hb, off, n_pieces_l), plan_last_.pieces.data(), n_pieces_l * sizeof(AttnPiece));
+    o_ctaoff_l = off;
+    std::memcpy(carve<uint32_t>(hb, off, n_items_l + 1), plan_last_.cta_off.data(), (n_items_l + 1) * sizeof(uint32_t));
+    o_rowc = off;
+    uint32_t* rowc = carve<uint32_t>(hb, off, 2 * n);  // [0, n): identity; [n, 2n): each request's last batch row
+    for (uint32_t r = 0; r < n; ++r) {
+      rowc[r] = r;
+      rowc[n + r] = rd[r].q_row0 + rd[r].n_q - 1;
+    }
+  }
+  if (off > need) { err = "engine: metadata layout overflow"; return MTKV_ERROR; }  // carve order == need order
   std::memcpy(h_req, rd.data(), nr * sizeof(ReqDev));
   if (!pages.empty()) std::memcpy(h_pages, pages.data(), pages.size() * sizeof(uint32_t));
   std::vector<uint32_t>& cands_k = slot_cands_[k];
@@ -794,8 +843,10 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     const size_t rb = size_t(rows) * d * sizeof(__nv_bfloat16);
     // comp-only workspaces: stream-ordered growth (no device synchronisation)
     if (x_.ensure(rb, comp_) || x2_.ensure(rb, comp_) || u_.ensure(rb, comp_) || q_.ensure(rb, comp_) ||
-        mid_.ensure(rb, comp_) || part_o_.ensure(size_t(plan_.n_slots) * part_slot_floats(bq, g_.D) * sizeof(float), comp_) ||
-        part_lse_.ensure(size_t(plan_.n_slots) * bq * sizeof(float), comp_) ||
+        mid_.ensure(rb, comp_) ||
+        part_o_.ensure(size_t(std::max(plan_.n_slots, reduce_last ? plan_last_.n_slots : 0u)) * part_slot_floats(bq, g_.D) *
+                           sizeof(float), comp_) ||
+        part_lse_.ensure(size_t(std::max(plan_.n_slots, reduce_last ? plan_last_.n_slots : 0u)) * bq * sizeof(float), comp_) ||
         logits_.ensure(size_t(nr) * V * sizeof(float), comp_) ||
         scores_.ensure(size_t(ncand_total) * sizeof(float), comp_)) {
       err = "engine: workspace alloc";
@@ -833,9 +884,16 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       if (prof) CK(cudaEventRecord(ev_attn_[2 * g_.L + 2 * l], comp_));
       if (gemm(ga, x_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       if (prof) CK(cudaEventRecord(ev_attn_[2 * g_.L + 2 * l + 1], comp_));
+      // the last layer (reduce_last): one query row per request, compact rows after it
+      const bool last = reduce_last && l + 1 == g_.L;
+      const uint32_t lrows = last ? n : rows;
+      const AttnSeg* segs_l = last ? reinterpret_cast<const AttnSeg*>(db + o_segs_l) : d_segs;
       AttnArgs aa{};
-      aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.reqs = d_req; aa.segs = d_segs; aa.items = d_items;
-      aa.n_items = n_items; aa.pieces = d_pieces; aa.cta_off = d_ctaoff;
+      aa.q = Q; aa.pool = pool; aa.pages = d_pages; aa.segs = segs_l; aa.items = d_items;
+      aa.reqs = last ? reinterpret_cast<const ReqDev*>(db + o_req_l) : d_req;
+      aa.n_items = last ? n_items_l : n_items;
+      aa.pieces = last ? reinterpret_cast<const AttnPiece*>(db + o_pieces_l) : d_pieces;
+      aa.cta_off = last ? reinterpret_cast<const uint32_t*>(db + o_ctaoff_l) : d_ctaoff;
       aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
       aa.g = g_; aa.layer = l; aa.bq = bq; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
@@ -866,22 +924,35 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l + 1], comp_));
       ++attn_launches_last_;
       GateArgs gn{};
-      gn.part_o = aa.part_o; gn.part_lse = aa.part_lse; gn.segs = d_segs; gn.bm = bq; gn.u = U; gn.ln_scale = w_ln_ + size_t(l) * d;
-      gn.row_req = d_rr; gn.reqs = d_req; gn.out = X2; gn.rows = rows; gn.H = H; gn.D = g_.D;
-      gn.blocks = reinterpret_cast<const uint32_t*>(db + o_gblk); gn.n_blocks = n_gblk;
+      gn.part_o = aa.part_o; gn.part_lse = aa.part_lse; gn.segs = segs_l; gn.bm = bq; gn.u = U; gn.ln_scale = w_ln_ + size_t(l) * d;
+      gn.out = X2; gn.rows = lrows; gn.H = H; gn.D = g_.D;
+      if (last) {  // compact row r <- request r's last row (row-per-warp kernel)
+        const uint32_t* rowc = reinterpret_cast<const uint32_t*>(db + o_rowc);
+        gn.reqs = reinterpret_cast<const ReqDev*>(db + o_req_g);
+        gn.row_req = rowc;
+        gn.u_rows = rowc + n;
+      } else {
+        gn.reqs = d_req;
+        gn.row_req = d_rr;
+        gn.blocks = reinterpret_cast<const uint32_t*>(db + o_gblk);
+        gn.n_blocks = n_gblk;
+      }
       launch_gate_norm(gn, comp_);
       GemmArgs m1{};
-      m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = rows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID; m1.pdl = true;
+      m1.A = X2; m1.B = w1_ + size_t(l) * d * d; m1.M = lrows; m1.N = d; m1.K = d; m1.epi = Epi::SiluBf16; m1.out = MID; m1.pdl = true;
       if (gemm(m1, x2_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       GemmArgs m2{};
-      m2.A = MID; m2.B = w2_ + size_t(l) * d * d; m2.M = rows; m2.N = d; m2.K = d; m2.epi = Epi::Bf16; m2.out = X; m2.pdl = true;
+      m2.A = MID; m2.B = w2_ + size_t(l) * d * d; m2.M = lrows; m2.N = d; m2.K = d; m2.epi = Epi::Bf16; m2.out = X; m2.pdl = true;
       if (gemm(m2, mid_.bytes / (size_t(d) * 2), err)) return MTKV_ERROR;
       launches += 5;
     }
+    // the final hidden row of request r: X[last_row[r]], or X[r] after a compact last layer
+    const uint32_t* lastrow = reduce_last ? reinterpret_cast<const uint32_t*>(db + o_rowc) : d_last;
     if (opt_.keep_logits || !w_out_t_) {
       // full-vocabulary logits (kept for the caller), candidates picked from them
       GemmArgs hd{};
-      hd.A = X; hd.row_idx = d_last; hd.B = w_out_; hd.M = nr; hd.N = V; hd.K = d; hd.epi = Epi::F32; hd.out = logits_.p;
+      hd.A = X; hd.row_idx = lastrow; hd.B = w_out_; hd.M = reduce_last ? n : nr; hd.N = V; hd.K = d; hd.epi = Epi::F32;
+      hd.out = logits_.p;
       launch_gemm(hd, comp_);
       ++launches;
       if (ncand_total) {
@@ -892,7 +963,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     } else if (ncand_total) {
       // serving: only the candidates' scores are ever read
       candidate_scores_kernel<<<(ncand_total + 7) / 8, 256, 0, comp_>>>(static_cast<float*>(scores_.p), X, w_out_t_,
-                                                                      d_last, d_creq, d_cid, ncand_total, d);
+                                                                      lastrow, d_creq, d_cid, ncand_total, d);
       ++launches;
     }
     if (calibrate_) CK(cudaEventRecord(ev_stk1_[k], comp_));

@@ -125,6 +125,7 @@ class Engine {
   double last_plan_ms_ = 0;
   uint64_t last_rows_ = 0;
   AttnPlan plan_;                // attention plan of the batch being enqueued
+  AttnPlan plan_last_;           // ... of its last layer (one query row per request)
   const char* trace_path_ = std::getenv("MTKV_ATTN_TRACE");
   DevBuf trace_;
   alignas(64) CUtensorMap pool_map_{};

@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
   if (row >= (int)a.rows) return;
   const ReqDev R = a.reqs[a.row_req[row]];
   const uint32_t i = row - R.q_row0, qt = i / a.bm, ri = i % a.bm, d = a.H * a.D;
+  const size_t urow = a.u_rows ? a.u_rows[row] : uint32_t(row);  // gate operand's batch row
   constexpr int NE = E > 0 ? E : GATE_MAXE;
   float x[NE];
   float sum = 0.f;
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
     // the gate operand does not depend on the merge: its load overlaps the slot reads
     float ug[E];
     {
-      const __nv_bfloat16* up = a.u + (size_t)row * d + j0;
+      const __nv_bfloat16* up = a.u + urow * d + j0;
       if constexpr (E % 8 == 0) {
 #pragma unroll
         for (int e = 0; e < E; e += 8) {
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(GATE_WARPS * 32) gate_norm_kernel(GateArgs a) 
       const uint32_t h = j / a.D;
       const AttnSeg sg = a.segs[R.seg0 + h * R.qtiles + qt];
       const float o = gate_merge_col(a, sg, ri, j % a.D);
-      x[e] = silu_f(o) * __bfloat162float(a.u[(size_t)row * d + j]);
+      x[e] = silu_f(o) * __bfloat162float(a.u[urow * d + j]);
       sum += x[e];
     }
   }

@@ -39,6 +39,8 @@ struct ReqDev {
   uint32_t user;
   uint64_t dep_start;   // keys >= dep_start may be appended by this batch's projection GEMM
                         // (the user's first occurrence in the batch; later occurrences read them)
+  uint32_t q_skip = 0;  // tcgen05 path: query rows [0, q_skip) are not computed (the last layer
+                        // needs only each request's last row: model.cpp:195 reads e[last])
 };
 
 // Attention work decomposition. A segment = (request, head, query tile of bm
@@ -59,7 +61,7 @@ struct alignas(16) AttnPiece {
   uint32_t seg, lo, hi, part;
   uint32_t head, qtile, q_row0, n_q;      // segment / request
   uint32_t n_hist, n_cand, pages_off, scratch_off;
-  uint32_t n_scratch, pad_;
+  uint32_t n_scratch, q_skip;            // q_skip: the tile's rows are q_skip + qtile * bm + r
   uint64_t start, dep_start;
 };
 struct AttnItem {  // mma.sync path: one CTA = (request, head, query tile, key split)
@@ -148,6 +150,9 @@ struct GateArgs {  // split combine + silu(o) * u + layer norm -> bf16 (launched
   // query rows of one request each, aligned to the bm-row query tiles
   const uint32_t* blocks = nullptr;
   uint32_t n_blocks = 0;
+  // optional: batch row of the gate operand u for output row `row` (the compact
+  // last layer: out row r <- request r's last row)
+  const uint32_t* u_rows = nullptr;
 };
 constexpr uint32_t kGateBlockRows = 32;
 bool gate_block_supported(uint32_t H, uint32_t D);
