@@ -79,7 +79,8 @@ CONFIGS = {
 def LAST_LAYER_REDUCED(cfg) -> bool:
     """The engine's tcgen05 attention path (head_dim 64/128, not forced to another
     kernel by MTKV_ATTN) runs the last layer for each request's last row only."""
-    return cfg["D"] in (64, 128) and os.environ.get("MTKV_ATTN", "") not in ("mma", "pp")
+    return (cfg["D"] in (64, 128) and os.environ.get("MTKV_ATTN", "") not in ("mma", "pp")
+            and not os.environ.get("MTKV_LAST_LAYER", "").startswith("f"))
 
 
 CONFIG_TAG = {"gr4_d256": "configs[1]", "tiny_d64": "configs[0]", "gr8_d512": "configs[3]"}
@@ -369,12 +370,16 @@ def run_b200(args, cfg):
         sm, sc, gm, gc = eng.last_chunk_copy_ms()
         copy_stat[0] += sm; copy_stat[1] += sc; copy_stat[2] += gm; copy_stat[3] += gc
         copy_stat[4] += 1 if sc else 0; copy_stat[5] += 1 if gc else 0
-        for p in eng.plans():
+        plans = eng.plans()
+        # the last layer computes only each request's last row (tcgen05 path,
+        # batches of >= 4096 fresh rows: engine.cu reduce_last)
+        reduced = LAST_LAYER_REDUCED(cfg) and sum(
+            p["fresh_history"] + p["delta"] + p["num_candidates"] for p in plans) >= 4096
+        for p in plans:
             keys = p["history_len"] + p["delta"] + p["num_candidates"]
             rows = p["fresh_history"] + p["delta"] + p["num_candidates"]
-            # per layer: K+V of every visible key once + Q (bf16) read + O (fp32) write;
-            # the last layer computes only each request's last row (tcgen05 path)
-            last_rows = 1 if LAST_LAYER_REDUCED(cfg) else rows
+            # per layer: K+V of every visible key once + Q (bf16) read + O (fp32) write
+            last_rows = 1 if reduced else rows
             attn_bytes += (cfg["L"] - 1) * (keys * d * 2 * 2 + rows * d * 2 + rows * d * 4)
             attn_bytes += keys * d * 2 * 2 + last_rows * d * 6
     eng.set_profile(False)

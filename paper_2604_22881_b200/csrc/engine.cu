@@ -593,7 +593,13 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   // for one row per request — none for a split host hit's re-encoded head.
   // rd_last: the requests with q_skip = n_q - 1; rd_gate: the same segments seen
   // from compact rows (row r = request r).
-  const bool reduce_last = value_ && attn_kind_ == AttnKind::Tc;
+  static const bool full_last = [] {  // MTKV_LAST_LAYER=full: every row through the last layer (A/B switch)
+    const char* e = std::getenv("MTKV_LAST_LAYER");
+    return e && e[0] == 'f';
+  }();
+  // (small batches are host-bound: the second attention plan costs more than
+  // the last layer's few rows; measured ~2.5 % on configs[0])
+  const bool reduce_last = value_ && attn_kind_ == AttnKind::Tc && !full_last && rows >= 4096;
   std::vector<ReqDev> rd_last, rd_gate;
   if (reduce_last) {
     rd_last.assign(rd.begin(), rd.begin() + n);
