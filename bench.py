@@ -389,7 +389,7 @@ def run_b200(args, cfg):
     # ---- phase C (e2e): public API with Python request dicts, every step's rankings read back ----
     # pipelined serving: batch i's rankings are read (D2H + host ranking) while
     # batches i+1 .. i+3 are in flight, as a server overlapping requests would
-    # (the engine keeps the results of its last 4 batches; depth 3 measured
+    # (the engine keeps the results of its last 6 batches; depth 3 measured
     # 17.4 K vs 12.7 K requests/s at depth 2: the next batch's onload must be
     # queued before the link drains, tools/probe_timing.py)
     e0 = eng.report()

@@ -200,7 +200,7 @@ int mtkv_engine_last_logits(mtkv_engine* e, float* out, uint32_t cap_rows);
 int mtkv_engine_last_rankings(mtkv_engine* e, uint32_t* out, uint64_t cap);
 /* Pipelined serving: rankings of an earlier batch, identified by its ticket
  * (0-based index among successfully submitted batches), while later batches are
- * still in flight; the last 4 submitted batches stay readable. Blocks until that
+ * still in flight; the last 6 submitted batches stay readable. Blocks until that
  * batch has completed. The reference returns each batch's results from
  * Engine::process_batch (sim.hpp:332); this splits submit and read-back so the
  * host can enqueue batch i+1's onload before reading batch i. */

@@ -104,6 +104,7 @@ Engine::Engine(const mtkv_kv_config& kv, const mtkv_cost_model& cost, const mtkv
   g_.num_pages = recompute_ ? 0 : kv.device_pages;
   chunk_elems_ = size_t(g_.L) * 2 * g_.chunk * g_.d;
   chunk_bytes_ = chunk_elems_ * sizeof(__nv_bfloat16);
+  for (int k = 0; k < kRing; ++k) scatter_batch_[k] = d2h_rec_batch_[k] = slot_batch_[k] = -1;
 }
 
 Engine::~Engine() {
@@ -650,10 +651,13 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
     meta_host_bytes_[k] = std::max(need, meta_host_bytes_[k] * 2);
     CK(cudaHostAlloc((void**)&meta_host_[k], meta_host_bytes_[k], cudaHostAllocDefault));
   }
-  if (meta_.ensure(need * kRing)) { err = "engine: metadata alloc"; return MTKV_ERROR; }
+  // one 256-B aligned device slot per ring entry (kernels read 16-B vectors from it)
+  if (need > meta_slot_) {
+    meta_slot_ = (std::max(need, 2 * meta_slot_) + 255) & ~size_t(255);
+    if (meta_.ensure(meta_slot_ * kRing)) { err = "engine: metadata alloc"; return MTKV_ERROR; }
+  }
   char* hb = meta_host_[k];
-  char* db = static_cast<char*>(meta_.p) + size_t(k) * (meta_.bytes / kRing);
-  if (need > meta_.bytes / kRing) { err = "engine: metadata ring overflow"; return MTKV_ERROR; }
+  char* db = static_cast<char*>(meta_.p) + size_t(k) * meta_slot_;
   size_t off = 0;
   ReqDev* h_req = carve<ReqDev>(hb, off, nr);
   const size_t o_pages = off;

@@ -26,7 +26,7 @@
 
 namespace mtkv_b200 {
 
-constexpr int kRing = 4;  // batches in flight on the device
+constexpr int kRing = 6;  // batches in flight on the device (and results kept for rankings)
 
 struct DevBuf {
   void* p = nullptr;
@@ -98,7 +98,7 @@ class Engine {
   // (embed -> scores) and the onload copies' span on h2d, with the rows / bytes
   // they processed; read back when the slot is reused (the batch is complete)
   cudaEvent_t ev_stk0_[kRing], ev_stk1_[kRing], ev_h2d0_[kRing], ev_h2d1_[kRing];
-  uint64_t cal_rows_[kRing] = {0, 0, 0, 0}, cal_bytes_[kRing] = {0, 0, 0, 0};
+  uint64_t cal_rows_[kRing] = {}, cal_bytes_[kRing] = {};
   double cal_tps_ = 0, cal_Bps_ = 0;  // EMAs (0: no measurement yet)
   bool calibrate_ = false;            // adaptive policy with no fixed rates given
   void calibrate_from(int k);
@@ -108,9 +108,9 @@ class Engine {
   uint32_t attn_launches_last_ = 0;
   uint64_t batch_no_ = 0;
   int64_t last_slot_ = -1;
-  bool have_scatter_[kRing] = {false, false, false, false};
-  bool have_d2h_[kRing] = {false, false, false, false};
-  int64_t scatter_batch_[kRing] = {-1, -1, -1, -1};
+  bool have_scatter_[kRing] = {};
+  bool have_d2h_[kRing] = {};
+  int64_t scatter_batch_[kRing];  // -1: none (constructor)
 
   // device memory
   DevBuf pool_, staging_[2], offload_, meta_, x_, x2_, u_, q_, mid_, part_o_, part_lse_, logits_, scores_;
@@ -154,20 +154,21 @@ class Engine {
   // ev_d2h_ slots are reused every kRing batches: a batch that left the ring has
   // its D2H confirmed on the host (d2h_done_upto_), so waits only ever target
   // batches still in the ring and never alias a newer record of the same slot
-  int64_t d2h_rec_batch_[kRing] = {-1, -1, -1, -1};  // batch that last recorded ev_d2h_[k]
+  int64_t d2h_rec_batch_[kRing];  // batch that last recorded ev_d2h_[k] (-1: none; constructor)
   int64_t d2h_done_upto_ = -1;
-  char* meta_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
-  size_t meta_host_bytes_[kRing] = {0, 0, 0, 0};
-  float* scores_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
-  size_t scores_host_bytes_[kRing] = {0, 0, 0, 0};
-  float* logits_host_[kRing] = {nullptr, nullptr, nullptr, nullptr};
-  size_t logits_host_bytes_[kRing] = {0, 0, 0, 0};
+  char* meta_host_[kRing] = {};
+  size_t meta_host_bytes_[kRing] = {};
+  size_t meta_slot_ = 0;  // bytes per ring slot of the device metadata buffer (256-B multiple)
+  float* scores_host_[kRing] = {};
+  size_t scores_host_bytes_[kRing] = {};
+  float* logits_host_[kRing] = {};
+  size_t logits_host_bytes_[kRing] = {};
 
   // last batch bookkeeping for logits / rankings
   uint32_t last_n_ = 0;
   // per ring slot: candidate ids and counts of the batch whose scores it holds
   std::vector<uint32_t> slot_cands_[kRing], slot_nc_[kRing];
-  int64_t slot_batch_[kRing] = {-1, -1, -1, -1};
+  int64_t slot_batch_[kRing];  // -1: none (constructor)
   uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0, onload_chunks_ = 0, offload_chunks_ = 0;
 };
 

@@ -193,7 +193,7 @@ def test_value_engine_rankings():
 def test_pipelined_rankings_match_synchronous():
     """submit()/rankings(ticket) with up to 3 batches in flight returns exactly the
     rankings of the synchronous process_batch()/last_rankings() path; tickets older
-    than the 4-batch result ring are refused."""
+    than the 6-batch result ring are refused."""
     case = [c for c in golden_cases("value") if c["name"] == "value10"][0]
     m = mtkv.ModelConfig(**case["model"])
     bs = batches(case["trace"], 2)

@@ -154,7 +154,7 @@ def main():
     eng.set_onload_policy("adaptive")
 
     # 2. e2e through submit / rankings at several pipeline depths
-    for depth in (1, 2, 3):
+    for depth in (3, 4, 5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pending, wait_s = [], 0.0
