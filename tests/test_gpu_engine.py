@@ -513,3 +513,59 @@ def test_value_payload_rejected_before_any_state_change():
         assert eng.state_blob() == before
     eng.process_batch([good])
     assert eng.state_blob() != before
+
+
+_LAST_LAYER_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2604_22881_b200 as mtkv
+from tests.test_gpu_engine import _last_layer_trace
+kv, mc, trace = _last_layer_trace()
+eng = mtkv.Engine(kv, mode="hierarchical", backend="value", batch_size=4, model=mc, keep_logits=True)
+out = []
+for i in range(0, len(trace), 4):
+    eng.process_batch(trace[i:i + 4])
+    out.append(np.asarray(eng.last_logits(), dtype=np.float64))
+np.save({path!r}, np.concatenate(out))
+"""
+
+
+def _last_layer_trace():
+    kv = _kv(dict(num_layers=3, num_heads=2, head_dim=128, page_size=32, chunk_size=128, device_pages=1200,
+                  offload_quota=128 * 32))
+    mc = mtkv.ModelConfig(num_layers=3, num_heads=2, head_dim=128, vocab=1024, seed=4)
+    rng = np.random.default_rng(3)
+    trace = []
+    for t in range(16):  # first visits of 1200 tokens (4 x 1208 rows per batch), then revisits
+        u = t % 8
+        dn = 1200 if t < 8 else int(rng.integers(900, 1300))
+        trace.append({"ts": t, "user": u, "dn": dn, "nc": 8, "tokens": rng.integers(0, 1024, dn).tolist(),
+                      "cands": rng.integers(0, 1024, 8).tolist()})
+    return kv, mc, trace
+
+
+def test_last_layer_one_row_per_request_matches_full_last_layer(tmp_path):
+    """Batches of >= 4096 rows run the last layer's attention / gate / MLP for
+    each request's last row only (engine.cu reduce_last): the logits must equal
+    those of the full last layer (MTKV_LAST_LAYER=full, in a child process) up
+    to fp32 summation order — the rows that reach the head compute the same."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = str(tmp_path / "full.npy")
+    r = subprocess.run([sys.executable, "-c", _LAST_LAYER_CHILD.format(root=root, path=path)],
+                       env={**os.environ, "MTKV_LAST_LAYER": "full"}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    full = np.load(path)
+    kv, mc, trace = _last_layer_trace()
+    eng = mtkv.Engine(kv, mode="hierarchical", backend="value", batch_size=4, model=mc, keep_logits=True)
+    got = []
+    for i in range(0, len(trace), 4):
+        eng.process_batch(trace[i:i + 4])
+        got.append(np.asarray(eng.last_logits(), dtype=np.float64))
+    got = np.concatenate(got)
+    assert got.shape == full.shape
+    rel = np.abs(got - full).max(axis=1) / np.abs(full).max(axis=1)
+    print(f"reduced vs full last layer: per-request max rel diff {rel.max():.3e}")
+    assert rel.max() <= 1e-2
