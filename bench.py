@@ -397,9 +397,10 @@ def run_b200(args, cfg):
     w0 = time.perf_counter()
     k1 = k0 + K
     pending, n_read, e2e_wait = [], 0, 0.0
+    depth = max(1, min(5, args.e2e_depth))
     for i in range(k1, k1 + K):
         pending.append(eng.submit(batches[i]))   # host dicts -> C-ABI (packing + H2D inside)
-        if len(pending) > 3:
+        if len(pending) > depth:
             wt = time.perf_counter()
             eng.rankings(pending.pop(0))
             e2e_wait += time.perf_counter() - wt
@@ -531,7 +532,7 @@ def run_b200(args, cfg):
         },
         "e2e": {"value": n_all / e2e_s, "unit": "requests/s", "h2d_bytes_per_step": phase_c["h2d_bytes_per_step"],
                 "d2h_bytes_per_step": phase_c["d2h_bytes_per_step"], "ms_per_step": e2e_s / K * 1e3,
-                "host_wait_ms_per_step": e2e_wait / K * 1e3,
+                "host_wait_ms_per_step": e2e_wait / K * 1e3, "depth": depth,
                 "timing": "host wall clock (perf_counter) around K pipelined submit + rankings calls, phase C"},
         "gpu_launches": int(round(launches_per_step * K)),
         "gpu_launches_per_step": launches_per_step,
@@ -643,6 +644,8 @@ def main():
     ap.add_argument("--onload-policy", default="adaptive", choices=["always", "adaptive"],
                     help="host hits: onload every persisted prefix (the reference's executor) or re-encode some "
                          "on the SMs while others stream over the host link (same control plane)")
+    ap.add_argument("--e2e-depth", type=int, default=3,
+                    help="phase C: batches kept in flight before reading the oldest one's rankings (<= 5: the engine keeps 6)")
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="configs[4] cache-pressure sweep: HBM pool as a fraction of the user population's KV")
     args = ap.parse_args()
