@@ -318,7 +318,9 @@ int mtkv_op_dense(void* out, const void* a, const void* w, uint32_t M, uint32_t 
  * batch (fresh history rows, candidates and cached prefix per request) for
  * `ctas` persistent CTAs and verifies every (request, head, query tile, key
  * tile) is covered exactly once and partial slots are contiguous. Returns 0 or
- * a failure code; out_stats[5] = {segments, pieces, tiles, max tiles per CTA, CTAs}. */
+ * a failure code; out_stats[5] = {segments, pieces, tiles, max tiles per CTA, CTAs}.
+ * tc: 0 = mma.sync items, 1 = one query tile per piece (attn_tc_kernel),
+ * 2 = paired query tiles (attn_pair_kernel; tiles counts key tiles streamed). */
 int mtkv_attention_plan_check(uint32_t n, const uint32_t* n_hist, const uint32_t* n_cand, const uint64_t* start,
                               uint32_t H, uint32_t D, uint32_t S, uint32_t ctas, int tc, uint32_t* out_stats);
 

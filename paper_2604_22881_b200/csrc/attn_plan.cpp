@@ -21,7 +21,8 @@
 
 namespace mtkv_b200 {
 
-void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& P) {
+void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& P, bool pair) {
+  P.pair = tc && pair;
   P.segs.clear();
   P.pieces.clear();
   P.cta_off.clear();
@@ -66,7 +67,9 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
     std::vector<std::vector<uint32_t>> lists(hg);
     std::vector<uint64_t> len(hg, 0);
     std::vector<std::vector<std::pair<uint32_t, uint32_t>>> spans(hg);  // (lo, hi) per listed segment
-    if (part == 2) {
+    // unit partner (paired kernel): B segment of each listed A segment, else kNoPart
+    std::vector<std::vector<uint32_t>> partner(hg);
+    if (part == 2 && !P.pair) {
       // alternate: segments in (request, head, query tile) order go to the
       // shorter of two lists, cut to even them out
       for (uint32_t sg = 0; sg < P.segs.size(); ++sg)
@@ -79,14 +82,20 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
           len[k] += take;
           lo += take;
         }
+      for (uint32_t k = 0; k < hg; ++k) partner[k].assign(lists[k].size(), kNoPart);
     } else {
+      // pair: query tiles (2j, 2j+1) of a (request, head) form one unit over
+      // the later tile's key tiles (the earlier one's are a prefix of them)
       for (uint32_t r = 0; r < n; ++r)
-        for (uint32_t qt = 0; qt < reqs[r].qtiles; ++qt)
+        for (uint32_t qt = 0; qt < reqs[r].qtiles; qt += P.pair ? 2 : 1)
           for (uint32_t h = 0; h < H; ++h) {
             const uint32_t sg = reqs[r].seg0 + h * reqs[r].qtiles + qt;
+            const bool two = P.pair && qt + 1 < reqs[r].qtiles;
+            const uint32_t nt = P.segs[two ? sg + 1 : sg].n_tiles;
             lists[h % hg].push_back(sg);
-            spans[h % hg].push_back({0, P.segs[sg].n_tiles});
-            len[h % hg] += P.segs[sg].n_tiles;
+            partner[h % hg].push_back(two ? sg + 1 : kNoPart);
+            spans[h % hg].push_back({0, nt});
+            len[h % hg] += nt;
           }
     }
     const uint64_t G = std::max<uint64_t>(hg, std::min<uint64_t>(ctas, total));
@@ -104,6 +113,8 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
           pc.seg = sg;
           pc.lo = lo;
           pc.hi = lo + take;
+          pc.part_b = partner[k][li];  // B's segment for now (its slot below)
+          pc.na = P.segs[sg].n_tiles;
           R[k][std::min(c, groups - 1)].push_back(pc);
           lo += take;
           room -= take;
@@ -118,7 +129,10 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
     // slots: a segment's pieces may sit in different CTAs' lists; give every
     // segment a contiguous slot range
     std::vector<uint32_t> npc(P.segs.size(), 0);
-    for (const AttnPiece& pc : P.pieces) ++npc[pc.seg];
+    for (const AttnPiece& pc : P.pieces) {
+      if (pc.lo < pc.na) ++npc[pc.seg];  // the A tile has key tiles in this piece
+      if (pc.part_b != kNoPart) ++npc[pc.part_b];
+    }
     for (uint32_t sg = 0; sg < P.segs.size(); ++sg) {
       P.segs[sg].part_base = P.n_slots;
       P.segs[sg].n_parts = npc[sg];
@@ -126,7 +140,8 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
     }
     std::vector<uint32_t> used(P.segs.size(), 0);
     for (AttnPiece& pc : P.pieces) {
-      pc.part = P.segs[pc.seg].part_base + used[pc.seg]++;
+      pc.part = pc.lo < pc.na ? P.segs[pc.seg].part_base + used[pc.seg]++ : kNoPart;
+      if (pc.part_b != kNoPart) pc.part_b = P.segs[pc.part_b].part_base + used[pc.part_b]++;
       const AttnSeg& sg = P.segs[pc.seg];
       const ReqDev& R = reqs[sg.req];
       pc.head = sg.head;
@@ -192,7 +207,7 @@ extern "C" int mtkv_attention_plan_check(uint32_t n, const uint32_t* n_hist, con
     rows += rq[r].n_q;
   }
   AttnPlan P;
-  plan_attention(rq.data(), n, g, tc != 0, ctas, P);
+  plan_attention(rq.data(), n, g, tc != 0, ctas, P, tc == 2);  // tc = 2: paired query tiles
   // every segment: its slots are contiguous and its tiles are covered exactly once
   std::vector<std::vector<uint32_t>> cover(P.segs.size());
   for (size_t s = 0; s < P.segs.size(); ++s) cover[s].assign(tc ? P.segs[s].n_tiles : 1, 0);
@@ -203,10 +218,22 @@ extern "C" int mtkv_attention_plan_check(uint32_t n, const uint32_t* n_hist, con
       uint64_t t = 0;
       for (uint32_t i = P.cta_off[c]; i < P.cta_off[c + 1]; ++i) {
         const AttnPiece& pc = P.pieces[i];
-        if (pc.seg >= P.segs.size() || pc.lo >= pc.hi || pc.hi > P.segs[pc.seg].n_tiles) return 2;
+        if (pc.seg >= P.segs.size() || pc.lo >= pc.hi) return 2;
         const AttnSeg& sg = P.segs[pc.seg];
-        if (pc.part < sg.part_base || pc.part + 1 > sg.part_base + sg.n_parts) return 3;
-        for (uint32_t x = pc.lo; x < pc.hi; ++x) ++cover[pc.seg][x];
+        const uint32_t ha = std::min(pc.hi, pc.na);
+        if (pc.lo < ha && (pc.part < sg.part_base || pc.part + 1 > sg.part_base + sg.n_parts)) return 3;
+        if (pc.lo >= ha && pc.part != kNoPart) return 3;
+        for (uint32_t x = pc.lo; x < ha; ++x) ++cover[pc.seg][x];
+        if (pc.part_b != kNoPart) {  // paired: B = the next query tile of the same (request, head)
+          const uint32_t sb = pc.seg + 1;
+          if (!P.pair || sb >= P.segs.size() || P.segs[sb].req != sg.req || P.segs[sb].head != sg.head ||
+              P.segs[sb].qtile != sg.qtile + 1 || pc.hi > P.segs[sb].n_tiles)
+            return 8;
+          if (pc.part_b < P.segs[sb].part_base || pc.part_b + 1 > P.segs[sb].part_base + P.segs[sb].n_parts) return 3;
+          for (uint32_t x = pc.lo; x < pc.hi; ++x) ++cover[sb][x];
+        } else if (pc.hi > sg.n_tiles) {
+          return 2;
+        }
         t += pc.hi - pc.lo;
       }
       tiles += t;

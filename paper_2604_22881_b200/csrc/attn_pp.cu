@@ -430,6 +430,7 @@ uint32_t attn_plan_ctas(AttnKind k, int n_sm) {
 void launch_attention_any(AttnKind k, const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a,
                           cudaStream_t s) {
   if (k == AttnKind::Pp) launch_attention_pp(pool_map, q_map, a, s);
+  else if (k == AttnKind::Tc && a.pair) launch_attention_pair(pool_map, q_map, a, s);
   else if (k == AttnKind::Tc) launch_attention_tc(pool_map, q_map, a, s);
   else launch_attention(a, s);
 }

@@ -371,10 +371,14 @@ __global__ void __launch_bounds__(384, 1)
         const int kb = int(t - P.lo) * BN;
         const int cu = min(max(ue - kb, 0), HC), c_lo = min(max(cl - kb, 0), HC), c_hi = min(max(ce - kb, 0), HC);
         if (cu != HC) {
+          // valid columns as a bit mask per 32-column chunk: one shift + select per
+          // element (a per-element || compiled to a divergent branch each)
 #pragma unroll
-          for (int c = 0; c < HC; ++c) {
-            const bool ok = c < cu || (c >= c_lo && c < c_hi);
-            s[c] = ok ? s[c] : -INFINITY;
+          for (int q = 0; q < (HC + 31) / 32; ++q) {
+            const int c0 = q * 32;
+            const uint32_t bits = range_bits(-c0, cu - c0) | range_bits(c_lo - c0, c_hi - c0);
+#pragma unroll
+            for (int c = 0; c < 32 && c0 + c < HC; ++c) s[c0 + c] = (bits >> c) & 1u ? s[c0 + c] : -INFINITY;
           }
         }
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};

@@ -585,7 +585,8 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
   }
   last_rows_ = rows;
   if (value_) {
-    plan_attention(rd.data(), nr, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_);
+    plan_attention(rd.data(), nr, g_, tc, attn_plan_ctas(attn_kind_, n_sm_), plan_,
+                   attn_kind_ == AttnKind::Tc && attn_pair_wanted(g_, rd.data(), nr));
     if (attn_kind_ == AttnKind::Pp && plan_.n_ctas() % 2) plan_.cta_off.push_back(plan_.cta_off.back());
   }
   // Last layer: the head reads only each request's last row (model.cpp:195
@@ -905,6 +906,7 @@ int Engine::enqueue(const BatchWork& w, const mtkv_request* reqs, uint32_t n, st
       aa.pieces = last ? reinterpret_cast<const AttnPiece*>(db + o_pieces_l) : d_pieces;
       aa.cta_off = last ? reinterpret_cast<const uint32_t*>(db + o_ctaoff_l) : d_ctaoff;
       aa.part_o = static_cast<float*>(part_o_.p); aa.part_lse = static_cast<float*>(part_lse_.p);
+      aa.pair = last ? 0u : uint32_t(plan_.pair);
       aa.g = g_; aa.layer = l; aa.bq = bq; aa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g_.D)));
       if (prof) CK(cudaEventRecord(ev_attn_[2 * l], comp_));
       if (tc && trace_path_ && l == 0) {  // MTKV_ATTN_TRACE: per-CTA timelines of layer 0

@@ -62,6 +62,8 @@ struct alignas(16) AttnPiece {
   uint32_t head, qtile, q_row0, n_q;      // segment / request
   uint32_t n_hist, n_cand, pages_off, scratch_off;
   uint32_t n_scratch, q_skip;            // q_skip: the tile's rows are q_skip + qtile * bm + r
+  uint32_t part_b = 0xFFFFFFFFu;         // paired kernel (attn_pair.cu): query tile qtile + 1's slot, or kNoPart
+  uint32_t na = 0xFFFFFFFFu;             // paired kernel: tile qtile attends key tiles < na only
   uint64_t start, dep_start;
 };
 struct AttnItem {  // mma.sync path: one CTA = (request, head, query tile, key split)
@@ -113,6 +115,8 @@ __host__ __device__ inline size_t part_index(uint32_t slot, uint32_t bm, uint32_
 }
 __host__ __device__ inline size_t part_slot_floats(uint32_t bm, uint32_t D) { return size_t(part_chunks(D)) * 4 * bm; }
 
+constexpr uint32_t kNoPart = 0xFFFFFFFFu;
+
 struct AttnArgs {
   const __nv_bfloat16* q;   // [rows x d]
   const __nv_bfloat16* pool;
@@ -131,6 +135,7 @@ struct AttnArgs {
   uint32_t bq;              // query rows per tile: 64 or 128 (items enumerate tiles of bq)
   unsigned long long* trace;  // optional per-CTA event timestamps (MTKV_ATTN_TRACE), else null
   uint32_t trigger = 1;       // tcgen05 path: release the PDL dependent (gate_norm) at CTA start
+  uint32_t pair = 0;          // tcgen05 path: the plan pairs query tiles (attn_pair_kernel)
 };
 constexpr int kTraceCtas = 64, kTraceTiles = 96, kTraceKinds = 12;
 void launch_attention(const AttnArgs& a, cudaStream_t s);
@@ -226,10 +231,18 @@ struct AttnPlan {
   std::vector<uint32_t> cta_off;   // tcgen05 path, n_ctas + 1 entries
   std::vector<AttnItem> items;     // mma.sync path
   uint32_t n_slots = 0;
+  bool pair = false;               // pieces are query-tile pairs (attn_pair_kernel)
   uint32_t n_ctas() const { return cta_off.empty() ? 0 : uint32_t(cta_off.size() - 1); }
 };
 constexpr uint32_t kTcBM = 128, kTcBN = 128;
 // Fills reqs[r].seg0/qtiles (and split_keys for the mma path) and the plan.
 // tcgen05: balanced contiguous key-tile ranges over `ctas` persistent CTAs.
-void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& plan);
+// pair: units of two query tiles (2j, 2j+1) of one (request, head) share their
+// key tiles (attn_pair_kernel, head_dim 128); a lone tile is a unit without B.
+void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& plan,
+                    bool pair = false);
+// the batch has a request with more than one query tile and the paired kernel applies
+bool attn_pair_wanted(const PoolGeom& g, const ReqDev* reqs, uint32_t n);
+void launch_attention_pair(const CUtensorMap& pool_map, const CUtensorMap& q_map, const AttnArgs& a,
+                           cudaStream_t s);
 }  // namespace mtkv_b200

@@ -113,7 +113,8 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
   const AttnKind kind = attn_kind(g);
   const bool tc = kind != AttnKind::Mma;
   AttnPlan plan;
-  plan_attention(rq.data(), n_req, g, tc, attn_plan_ctas(kind, num_sms()), plan);
+  plan_attention(rq.data(), n_req, g, tc, attn_plan_ctas(kind, num_sms()), plan,
+                 kind == AttnKind::Tc && attn_pair_wanted(g, rq.data(), n_req));
   if (kind == AttnKind::Pp && plan.n_ctas() % 2) plan.cta_off.push_back(plan.cta_off.back());
   const uint32_t n_items = tc ? plan.n_ctas() : uint32_t(plan.items.size());
   // one device allocation: requests | rows | segments | items or pieces + CTA offsets | lse | partials
@@ -155,6 +156,7 @@ static int attention_batch(float* out, const void* q, const void* pool, const ui
   a.g = g;
   a.layer = layer;
   a.bq = plan.bm;
+  a.pair = plan.pair;
   a.scale_log2 = float(1.4426950408889634 / sqrt(double(g.D)));
   if (e == cudaSuccess) {
     alignas(64) CUtensorMap pmap, qmap;

@@ -87,6 +87,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
       : "memory");
 }
+// L2 prefetch of one TMA box (no shared memory, no barrier): hides DRAM latency
+// for tiles further ahead than the shared-memory ring reaches
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
                "r"(c1), "r"(s32(src))
@@ -135,6 +141,14 @@ __device__ __forceinline__ void mma_ts_if(bool on, uint32_t d_tmem, uint32_t a_t
       "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
       "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(uint32_t(on))
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_if(bool on, uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(uint32_t(on))
       : "memory");
 }
 __device__ __forceinline__ void mma_commit_if(bool on, uint64_t* bar) {
@@ -207,6 +221,15 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 
 // byte offset of 16-byte chunk `c` (of 8) in row `r` of a SW128 K-major block
 __device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
+
+// bits [lo, hi) of a 32-column chunk (bounds clamped to [0, 32])
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi) {
+  lo = min(max(lo, 0), 32);
+  hi = min(max(hi, 0), 32);
+  const uint32_t top = hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u);
+  const uint32_t bot = lo >= 32 ? 0xFFFFFFFFu : ((1u << lo) - 1u);
+  return hi > lo ? top & ~bot : 0u;
+}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;

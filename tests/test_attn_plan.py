@@ -45,3 +45,27 @@ def test_plan_bench_batch_balanced():
 
 def test_plan_mma_path_items():
     _check([5, 100, 0], [1, 3, 8], [0, 500, 7], H=2, D=32, S=8, tc=0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_paired_plan_covers_every_tile_once(seed):
+    """Paired query tiles (attn_pair_kernel): every tile of both segments of a
+    unit is covered exactly once, the B slot belongs to the next query tile of
+    the same (request, head), and A only takes the key tiles it can see."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 40))
+    # prefill-shaped (many query tiles) mixed with decode-shaped requests
+    n_hist = np.where(rng.random(n) < 0.5, rng.integers(129, 4200, n), rng.integers(0, 200, n))
+    n_cand = rng.integers(1, 9, n)
+    start = np.where(rng.random(n) < 0.5, 0, rng.integers(0, 9000, n))
+    for H, S, ctas in ((2, 32, 148), (1, 64, 7), (4, 16, 148)):
+        segs, pieces, tiles, max_cta, nctas = (int(x) for x in _check(n_hist, n_cand, start, H=H, S=S, ctas=ctas, tc=2))
+        assert nctas <= ctas and max_cta * nctas >= tiles
+        assert max_cta <= 2 * -(-tiles // nctas) + 1
+
+
+def test_paired_plan_halves_key_tiles_of_a_prefill():
+    """A 4 K causal prefill: pairing streams each key tile once per two query tiles."""
+    single = _check([4096] * 8, [8] * 8, [0] * 8, tc=1)
+    paired = _check([4096] * 8, [8] * 8, [0] * 8, tc=2)
+    assert paired[2] < 0.56 * single[2]

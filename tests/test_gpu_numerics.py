@@ -78,7 +78,9 @@ SHAPES = [(2, 128, 32, 1000, 72), (4, 64, 16, 0, 130), (1, 32, 8, 333, 5), (2, 1
           (1, 8, 4, 17, 3), (2, 128, 64, 20000, 72), (4, 128, 32, 5000, 300), (1, 64, 8, 3000, 1),
           (3, 128, 16, 777, 129), (2, 64, 64, 0, 1000), (2, 128, 32, 4096, 200),
           # head_dim 32 on the tcgen05 kernel (d % 64 == 0): odd heads sit 64 B into a block
-          (2, 32, 16, 500, 40), (4, 32, 32, 3000, 130), (2, 32, 8, 0, 300), (6, 32, 32, 1100, 1)]
+          (2, 32, 16, 500, 40), (4, 32, 32, 3000, 130), (2, 32, 8, 0, 300), (6, 32, 32, 1100, 1),
+          # prefill-shaped (more than one 128-row query tile, head_dim 128; also run on the paired kernel)
+          (2, 128, 32, 0, 1000), (2, 128, 32, 0, 4100), (1, 128, 64, 300, 700), (2, 128, 16, 129, 257)]
 
 
 @pytest.mark.parametrize("H,D,S,p_pre,n_q", SHAPES)
@@ -258,6 +260,20 @@ def test_two_lane_attention_kernel_same_bars():
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_numerics.py"), "-q", "-x",
                         "-p", "no:cacheprovider", "-k", "relative_bar and not -32-"],
                        env={**os.environ, "MTKV_ATTN": "pp"}, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-400:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_paired_attention_kernel_same_bars():
+    """MTKV_ATTN_PAIR=1: the head_dim-128 shapes on the paired-query-tile kernel
+    (attn_pair.cu, a measured variant) against the same bars (the kernel choice
+    is fixed per process: child process)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_numerics.py"), "-q", "-x",
+                        "-p", "no:cacheprovider", "-k", "relative_bar and -128-"],
+                       env={**os.environ, "MTKV_ATTN_PAIR": "1"}, capture_output=True, text=True, timeout=600)
     print(r.stdout[-400:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
