@@ -343,6 +343,36 @@ def run_b200(args, cfg):
     launches_per_step = (eng.kernel_launches() - l0) / K
     phase_a = _phase(r0, r1, K, B)
 
+    # ---- phase C (e2e): public API with Python request dicts, every step's rankings read back ----
+    # (right after phase A: the adaptive policy's calibrated rates are phase A's;
+    # phase B runs the `always` policy with per-launch events)
+    # pipelined serving: batch i's rankings are read (D2H + host ranking) while
+    # batches i+1 .. i+depth are in flight, as a server overlapping requests
+    # would (the engine keeps the results of its last 6 batches; the next
+    # batch's onload must be queued before the link drains: depth 3 measured
+    # 17.4 K vs 12.7 K requests/s at depth 2, tools/probe_timing.py; default 5)
+    e0 = eng.report()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    kc = warm + K
+    pending, n_read, e2e_wait = [], 0, 0.0
+    depth = max(1, min(5, args.e2e_depth))
+    for i in range(kc, kc + K):
+        pending.append(eng.submit(batches[i]))   # host dicts -> C-ABI (packing + H2D inside)
+        if len(pending) > depth:
+            wt = time.perf_counter()
+            eng.rankings(pending.pop(0))
+            e2e_wait += time.perf_counter() - wt
+            n_read += 1
+    for t in pending:
+        eng.rankings(t)
+        n_read += 1
+    eng.synchronize()
+    e2e_s = time.perf_counter() - w0
+    assert n_read == K
+    phase_c = _phase(e0, eng.report(), K, B)
+
+
     # ---- phase B: per-batch device latency (p50/p99) + per-launch attention timing ----
     # (host hits onloaded: the incremental attention the roofline describes; the
     # adaptive policy's re-encoded prefixes are prefill-shaped, tensor-bound rows)
@@ -354,7 +384,7 @@ def run_b200(args, cfg):
     proj_stat = [0.0, 0, 0]  # projection GEMM ms, launches, rows (summed over launches)
     d = cfg["H"] * cfg["D"]
     rb0 = eng.report()
-    k0 = warm + K
+    k0 = warm + 2 * K
     for i in range(k0, k0 + K):
         eng.process_batch(None, packed=packed[i])
         eng.synchronize()
@@ -386,33 +416,7 @@ def run_b200(args, cfg):
     eng.set_onload_policy(args.onload_policy)
     phase_b = _phase(rb0, eng.report(), K, B)
 
-    # ---- phase C (e2e): public API with Python request dicts, every step's rankings read back ----
-    # pipelined serving: batch i's rankings are read (D2H + host ranking) while
-    # batches i+1 .. i+3 are in flight, as a server overlapping requests would
-    # (the engine keeps the results of its last 6 batches; depth 3 measured
-    # 17.4 K vs 12.7 K requests/s at depth 2: the next batch's onload must be
-    # queued before the link drains, tools/probe_timing.py)
-    e0 = eng.report()
-    torch.cuda.synchronize()
-    w0 = time.perf_counter()
-    k1 = k0 + K
-    pending, n_read, e2e_wait = [], 0, 0.0
-    depth = max(1, min(5, args.e2e_depth))
-    for i in range(k1, k1 + K):
-        pending.append(eng.submit(batches[i]))   # host dicts -> C-ABI (packing + H2D inside)
-        if len(pending) > depth:
-            wt = time.perf_counter()
-            eng.rankings(pending.pop(0))
-            e2e_wait += time.perf_counter() - wt
-            n_read += 1
-    for t in pending:
-        eng.rankings(t)
-        n_read += 1
-    eng.synchronize()
-    e2e_s = time.perf_counter() - w0
-    assert n_read == K
-    phase_c = _phase(e0, eng.report(), K, B)
-
+    k1 = k0  # phase D / E batches follow phase B's
     # ---- phase D (untimed): compute / transfer overlap of the next batches under CUPTI ----
     overlap, cupti_copy = None, {}
     try:
@@ -644,7 +648,7 @@ def main():
     ap.add_argument("--onload-policy", default="adaptive", choices=["always", "adaptive"],
                     help="host hits: onload every persisted prefix (the reference's executor) or re-encode some "
                          "on the SMs while others stream over the host link (same control plane)")
-    ap.add_argument("--e2e-depth", type=int, default=3,
+    ap.add_argument("--e2e-depth", type=int, default=5,
                     help="phase C: batches kept in flight before reading the oldest one's rankings (<= 5: the engine keeps 6)")
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="configs[4] cache-pressure sweep: HBM pool as a fraction of the user population's KV")
