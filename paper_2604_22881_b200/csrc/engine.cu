@@ -461,7 +461,14 @@ void Engine::calibrate_from(int k) {
   }
   cal_rows_[k] = cal_bytes_[k] = 0;
   (void)cudaGetLastError();  // an unavailable timing is skipped, not an engine error
-  if (cal_tps_ > 0 && cal_Bps_ > 0) planner.set_onload_policy(int(opt_.onload_policy), cal_Bps_, cal_tps_);
+  // MTKV_ADAPTIVE_SM_BIAS (A/B knob): scales the measured layer-stack rate
+  // before the split (its event bracket also spans waits on onloads)
+  static const double bias = [] {
+    const char* e = std::getenv("MTKV_ADAPTIVE_SM_BIAS");
+    const double v = e ? std::atof(e) : 1.0;
+    return v > 0.25 && v < 4.0 ? v : 1.0;
+  }();
+  if (cal_tps_ > 0 && cal_Bps_ > 0) planner.set_onload_policy(int(opt_.onload_policy), cal_Bps_, cal_tps_ * bias);
 }
 
 int Engine::process_batch(const mtkv_request* reqs, uint32_t n, std::string& err) {
