@@ -337,6 +337,8 @@ def run_b200(args, cfg):
     torch.cuda.nvtx.range_pop()
     t_end.record()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     clk = clocks.stop()
     r1 = eng.report()
     elapsed = t_start.elapsed_time(t_end) / 1e3
@@ -353,6 +355,8 @@ def run_b200(args, cfg):
     # 17.4 K vs 12.7 K requests/s at depth 2, tools/probe_timing.py; default 5)
     e0 = eng.report()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     w0 = time.perf_counter()
     kc = warm + K
     pending, n_read, e2e_wait = [], 0, 0.0
@@ -369,6 +373,8 @@ def run_b200(args, cfg):
         n_read += 1
     eng.synchronize()
     e2e_s = time.perf_counter() - w0
+    if dist:
+        dist.barrier()
     assert n_read == K
     phase_c = _phase(e0, eng.report(), K, B)
 
