@@ -14,12 +14,15 @@
 // mma.sync path (head_dim < 64): one CTA per (request, head, query tile, key
 // split of split_keys positions), one slot per split.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
 #include "kernels.cuh"
 
 namespace mtkv_b200 {
+
+constexpr double kPieceCostDefault = 2.0;
 
 void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32_t ctas, AttnPlan& P, bool pair) {
   P.pair = tc && pair;
@@ -100,24 +103,38 @@ void plan_attention(ReqDev* reqs, uint32_t n, const PoolGeom& g, bool tc, uint32
     }
     const uint64_t G = std::max<uint64_t>(hg, std::min<uint64_t>(ctas, total));
     const uint32_t groups = uint32_t(G / hg);
-    const uint64_t quota = (*std::max_element(len.begin(), len.end()) + groups - 1) / groups;
+    // Ranges are cut by cost, not tiles: a piece costs its tiles plus a fixed
+    // overhead (its Q load, pipeline refill and O/lse epilogue: measured ~2.7 us
+    // = ~2.2 tiles on a prefill, where a CTA's end time tracked its piece count
+    // with r = 0.98 under tile-count cutting). MTKV_ATTN_PIECE_COST (in tiles;
+    // 0 = tile-count cutting) is the A/B switch.
+    static const double pe_cost = [] {
+      const char* e = std::getenv("MTKV_ATTN_PIECE_COST");
+      const double v = e ? std::atof(e) : kPieceCostDefault;
+      return v >= 0.0 && v < 64.0 ? v : kPieceCostDefault;
+    }();
+    double max_cost = 0;
+    for (uint32_t k = 0; k < hg; ++k) max_cost = std::max(max_cost, double(len[k]) + pe_cost * double(lists[k].size()));
+    // every CTA boundary may split one segment (one more piece)
+    const double quota = std::ceil((max_cost + pe_cost * groups) / groups);
     std::vector<std::vector<std::vector<AttnPiece>>> R(hg, std::vector<std::vector<AttnPiece>>(groups));
     for (uint32_t k = 0; k < hg; ++k) {
       uint32_t c = 0;
-      uint64_t room = quota;
+      double room = quota;
       for (size_t li = 0; li < lists[k].size(); ++li)
         for (uint32_t sg = lists[k][li], lo = spans[k][li].first, hi = spans[k][li].second; lo < hi;) {
-          if (room == 0) { ++c; room = quota; }
-          const uint32_t take = uint32_t(std::min<uint64_t>(hi - lo, room));
+          if (room < pe_cost + 1.0 && c + 1 < groups) { ++c; room = quota; }
+          const uint32_t take = c + 1 == groups ? hi - lo
+              : uint32_t(std::min<double>(hi - lo, std::max(1.0, std::floor(room - pe_cost))));
           AttnPiece pc{};
           pc.seg = sg;
           pc.lo = lo;
           pc.hi = lo + take;
           pc.part_b = partner[k][li];  // B's segment for now (its slot below)
           pc.na = P.segs[sg].n_tiles;
-          R[k][std::min(c, groups - 1)].push_back(pc);
+          R[k][c].push_back(pc);
           lo += take;
-          room -= take;
+          room -= take + pe_cost;
         }
     }
     P.cta_off.push_back(0);
