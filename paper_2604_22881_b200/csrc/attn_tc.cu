@@ -340,6 +340,45 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t o_col = tmem + lane_base + C::O_COL + wg * (D / 2);
     uint32_t t_all = 0;      // tiles processed (barrier phases)
     auto named_sync = [&]() { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    // A piece's epilogue (O / l and lse into its slot) is deferred into the next
+    // piece's first tile, after that tile's exponentials and before its P is
+    // released: the wait for the piece's last PV then overlaps softmax work, and
+    // O / L are still read before the next piece's first PV (issued after that
+    // p_full) overwrites them. The CTA's last piece is written after the loop.
+    bool ep_pend = false, ep_valid = false;
+    uint32_t ep_part = 0, ep_pc = 0;
+    float ep_mref = 0.f;
+    auto epilogue = [&]() {  // the pending piece's last PV has completed
+      if (threadIdx.x == 128) ATTN_TR(11, 4 * (ep_pc - pb));
+      const float l_run = tmem_ld1(tmem + lane_base + C::L_COL);  // row sum of P (all 16 columns equal)
+      tmem_wait_ld();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (threadIdx.x == 128) ATTN_TR(11, 4 * (ep_pc - pb) + 1);
+      // O/l straight from TMEM to the slot: thread r owns row r's D/2 columns of
+      // this half; in the chunked slot layout (part_index) a warp's store of
+      // one 4-column chunk covers 32 consecutive rows = 512 contiguous bytes.
+      // Rows past the tile's valid rows are not written (the combine never
+      // reads them).
+      constexpr int CW = D / 2 >= 32 ? 32 : D / 2;  // columns per tcgen05.ld
+      float* dst = a.part_o + part_index(ep_part, BM, r, wg * (D / 2), D);
+      constexpr size_t chunk_stride = size_t(BM) * 4;  // floats between consecutive 4-column chunks
+#pragma unroll 1
+      for (int c = 0; c < D / 2 / CW; ++c) {
+        float o[CW];
+        if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
+        else tmem_ld16(o_col + c * CW, o);
+        tmem_wait_ld();
+        if (ep_valid) {
+#pragma unroll
+          for (int k = 0; k < CW / 4; ++k)
+            *reinterpret_cast<float4*>(dst + (c * CW / 4 + k) * chunk_stride) =
+                make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
+        }
+      }
+      if (wg == 0 && ep_valid) a.part_lse[size_t(ep_part) * BM + r] = l_run > 0.f ? ep_mref + log2f(l_run) : -INFINITY;
+      if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (ep_pc - pb));
+      ep_pend = false;
+    };
     for (uint32_t pc = pb; pc < pe; ++pc) {
       const AttnPiece P = a.pieces[pc];
       const uint64_t KA = P.start + P.n_hist;
@@ -436,6 +475,11 @@ __global__ void __launch_bounds__(384, 1)
               tmem_st16(o_col, w);
             }
           }
+        } else if (ep_pend) {  // the previous piece's epilogue (its last PV is tile t_all - 1)
+          if (threadIdx.x == 128) ATTN_TR(5, 3 + 2 * (ep_pc - pb));
+          mbar_wait(o_done, (t_all - 1) & 1);
+          tc_after();
+          epilogue();
         }
         if (threadIdx.x % 128 == 0) ATTN_TR(8, t_all);
         tmem_wait_st();
@@ -444,45 +488,18 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) mbar_arrive(p_full);
         if (threadIdx.x % 128 == 0) ATTN_TR(4, t_all);
       }
-      // ---- epilogue: O / l and lse (base 2) into slot `part` ----
-      if (threadIdx.x == 128) ATTN_TR(5, 3 + 2 * (pc - pb));
-      const uint32_t qi = q0 + r;
+      // ---- epilogue (O / l and lse into slot P.part): deferred, see above ----
+      ep_pend = true;
+      ep_part = P.part;
+      ep_valid = q0 + r < q_end;
+      ep_mref = m_ref;
+      ep_pc = pc;
+    }
+    if (ep_pend) {  // the CTA's last piece
+      if (threadIdx.x == 128) ATTN_TR(5, 3 + 2 * (ep_pc - pb));
       mbar_wait(o_done, (t_all - 1) & 1);
       tc_after();
-      if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb));
-      const float l_run = tmem_ld1(tmem + lane_base + C::L_COL);  // row sum of P (all 16 columns equal)
-      tmem_wait_ld();
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      if (threadIdx.x == 128) ATTN_TR(11, 4 * (pc - pb) + 1);
-      // O/l straight from TMEM to the slot: thread r owns row r's D/2 columns of
-      // this half; in the chunked slot layout (part_index) a warp's store of
-      // one 4-column chunk covers 32 consecutive rows = 512 contiguous bytes.
-      // Rows past the tile's valid rows are not written (the combine never
-      // reads them).
-      {
-        constexpr int CW = D / 2 >= 32 ? 32 : D / 2;  // columns per tcgen05.ld
-        float* dst = a.part_o + part_index(P.part, BM, r, wg * (D / 2), D);
-        constexpr size_t chunk_stride = size_t(BM) * 4;  // floats between consecutive 4-column chunks
-        const bool valid = qi < q_end;
-#pragma unroll 1
-        for (int c = 0; c < D / 2 / CW; ++c) {
-          float o[CW];
-          if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
-          else tmem_ld16(o_col + c * CW, o);
-          tmem_wait_ld();
-          if (valid) {
-#pragma unroll
-            for (int k = 0; k < CW / 4; ++k)
-              *reinterpret_cast<float4*>(dst + (c * CW / 4 + k) * chunk_stride) =
-                  make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
-          }
-        }
-      }
-      const size_t prow = size_t(P.part) * BM + r;
-      if (wg == 0 && qi < q_end) a.part_lse[prow] = l_run > 0.f ? m_ref + log2f(l_run) : -INFINITY;
-      if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (pc - pb));
-      // O is overwritten by the next piece's first PV (issued after p_full of
-      // its first tile, which this thread signals after the loads above)
+      epilogue();
       tc_before();
     }
     if (threadIdx.x == 128) ATTN_TR(5, 2);
