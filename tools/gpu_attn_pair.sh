@@ -1,7 +1,7 @@
 #!/bin/bash
 # paired kernel (MTKV_ATTN_PAIR=1): watchdog build + bars, then timing build: traced prefill, prefill / decode vs one-tile
 set -u
-O=gpurun_out/${1:-pair4}
+O=gpurun_out/${1:-attn_pair}
 mkdir -p $O
 export MTKV_ATTN_PAIR=1
 MTKV_NVCC_EXTRA=-DMTKV_WATCHDOG timeout 600 python -m paper_2604_22881_b200.build --force > $O/build_wd.log 2>&1
