@@ -350,30 +350,30 @@ __global__ void __launch_bounds__(384, 1)
     float ep_mref = 0.f;
     auto epilogue = [&]() {  // the pending piece's last PV has completed
       if (threadIdx.x == 128) ATTN_TR(11, 4 * (ep_pc - pb));
-      const float l_run = tmem_ld1(tmem + lane_base + C::L_COL);  // row sum of P (all 16 columns equal)
-      tmem_wait_ld();
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      if (threadIdx.x == 128) ATTN_TR(11, 4 * (ep_pc - pb) + 1);
       // O/l straight from TMEM to the slot: thread r owns row r's D/2 columns of
       // this half; in the chunked slot layout (part_index) a warp's store of
       // one 4-column chunk covers 32 consecutive rows = 512 contiguous bytes.
       // Rows past the tile's valid rows are not written (the combine never
-      // reads them).
-      constexpr int CW = D / 2 >= 32 ? 32 : D / 2;  // columns per tcgen05.ld
+      // reads them). L and this half of O are loaded with one wait.
+      constexpr int OC = D / 2;  // O columns of this half
+      float o[OC];
+      const float l_run = tmem_ld1(tmem + lane_base + C::L_COL);  // row sum of P (all 16 columns equal)
+      if constexpr (OC >= 32) {
+#pragma unroll
+        for (int c = 0; c < OC / 32; ++c) tmem_ld32(o_col + c * 32, o + c * 32);
+      } else {
+        tmem_ld16(o_col, o);
+      }
+      tmem_wait_ld();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (threadIdx.x == 128) ATTN_TR(11, 4 * (ep_pc - pb) + 1);
       float* dst = a.part_o + part_index(ep_part, BM, r, wg * (D / 2), D);
       constexpr size_t chunk_stride = size_t(BM) * 4;  // floats between consecutive 4-column chunks
-#pragma unroll 1
-      for (int c = 0; c < D / 2 / CW; ++c) {
-        float o[CW];
-        if constexpr (CW == 32) tmem_ld32(o_col + c * CW, o);
-        else tmem_ld16(o_col + c * CW, o);
-        tmem_wait_ld();
-        if (ep_valid) {
+      if (ep_valid) {
 #pragma unroll
-          for (int k = 0; k < CW / 4; ++k)
-            *reinterpret_cast<float4*>(dst + (c * CW / 4 + k) * chunk_stride) =
-                make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
-        }
+        for (int k = 0; k < OC / 4; ++k)
+          *reinterpret_cast<float4*>(dst + k * chunk_stride) =
+              make_float4(o[4 * k] * inv, o[4 * k + 1] * inv, o[4 * k + 2] * inv, o[4 * k + 3] * inv);
       }
       if (wg == 0 && ep_valid) a.part_lse[size_t(ep_part) * BM + r] = l_run > 0.f ? ep_mref + log2f(l_run) : -INFINITY;
       if (threadIdx.x == 128) ATTN_TR(5, 4 + 2 * (ep_pc - pb));
